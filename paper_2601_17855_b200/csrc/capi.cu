@@ -1,0 +1,554 @@
+// C ABI of the batched step engine (include/bfsim_gpu.h): context, scenario
+// validation (mirroring the reference's exceptions), launch planning and the
+// host <-> device plumbing. No exception crosses this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "bfsim_gpu.h"
+#include "common.h"
+#include "engine.cuh"
+
+using bfsim::fail;
+using bfsim::KParams;
+using bfsim::Plan;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) n = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+constexpr int kMaxGroups = 16;
+
+}  // namespace
+
+struct bfsim_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int smem_optin = 0;
+  cudaStream_t side[kMaxGroups] = {};
+  cudaEvent_t fork = nullptr, join[kMaxGroups] = {}, t0 = nullptr, t1 = nullptr;
+  // device buffers for the host-pointer entry
+  DevBuf scen, inputs, cbase, traces, streams, results, st_cs, st_dt, st_mx, st_ac, st_ld, rq_as,
+      rq_ss, rq_wk, rq_ac, rq_fc;
+  // planner-owned buffers
+  DevBuf order, ws, queue;
+  int64_t last_launches = 0;
+  bool timed = false;
+};
+
+namespace {
+
+int cuda_fail(char* err, size_t errlen, cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  return fail(err, errlen, BFSIM_ECUDA, m.c_str());
+}
+
+bool is_int_drift(double v) { return v >= 0.0 && v == std::floor(v) && v < 1e9; }
+
+// SimConfig::validate (engine.hpp:31-36), PowerModel::validate
+// (metrics_power.hpp:17-21), DriftSpec::validate (workload.hpp:52-60), plus the
+// GPU path's own limits. Returns a BFSIM_* code.
+int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, int32_t n_inputs,
+                      const std::vector<int>* single_class_inputs, char* err, size_t errlen) {
+  if (s.workers < 1 || s.batch < 1)
+    return fail(err, errlen, BFSIM_EINVAL, "config: workers and batch must be >= 1");
+  if (s.overhead < 0.0 || s.per_token <= 0.0)
+    return fail(err, errlen, BFSIM_EINVAL, "config: bad time constants");
+  if (s.horizon < 0 || (s.mode == BFSIM_MODE_POISSON && s.max_steps < 1))
+    return fail(err, errlen, BFSIM_EINVAL, "config: bad horizon or max_steps");
+  if (!(s.p_idle > 0.0 && s.p_idle < s.p_max))
+    return fail(err, errlen, BFSIM_EINVAL, "power: need 0 < p_idle < p_max");
+  if (!(s.mfu_sat > 0.0 && s.mfu_sat <= 1.0))
+    return fail(err, errlen, BFSIM_EINVAL, "power: mfu_sat out of (0,1]");
+  if (!(s.gamma > 0.0 && s.gamma < 1.0))
+    return fail(err, errlen, BFSIM_EINVAL, "power: gamma out of (0,1)");
+  if (s.drift < 0.0) return fail(err, errlen, BFSIM_EINVAL, "drift: increment out of [0, delta_max]");
+  if (!is_int_drift(s.drift))
+    return fail(err, errlen, BFSIM_EINVAL,
+                "drift: the GPU path is bit-exact only for integer constant drift (SURVEY F5)");
+  if (s.policy == BFSIM_POLICY_BFIO_EXACT)
+    return fail(err, errlen, BFSIM_EINVAL,
+                "bfio-exact is an exponential search; it runs on the CPU reference only");
+  if (s.policy != BFSIM_POLICY_FCFS && s.policy != BFSIM_POLICY_JSQ &&
+      s.policy != BFSIM_POLICY_BFIO_GREEDY)
+    return fail(err, errlen, BFSIM_EINVAL, "unknown policy");
+  if (s.mode != BFSIM_MODE_POISSON && s.mode != BFSIM_MODE_OVERLOADED)
+    return fail(err, errlen, BFSIM_EINVAL, "unknown mode");
+  if (s.lookahead < 0 || s.lookahead > 2) return fail(err, errlen, BFSIM_EINVAL, "unknown lookahead");
+  if (s.lookahead == BFSIM_LOOKAHEAD_NOISY && s.policy == BFSIM_POLICY_BFIO_GREEDY &&
+      s.mode == BFSIM_MODE_POISSON && s.noise_sigma > 0.0)
+    return fail(err, errlen, BFSIM_EINVAL, "noisy lookahead is not yet supported on the GPU path");
+  if (s.input_id < 0 || s.input_id >= n_inputs)
+    return fail(err, errlen, BFSIM_EINVAL, "scenario: input_id out of range");
+  if (s.workers > 256) return fail(err, errlen, BFSIM_EINVAL, "GPU path: workers > 256 not supported yet");
+  if (s.batch > 65535) return fail(err, errlen, BFSIM_EINVAL, "GPU path: batch > 65535");
+  if (static_cast<int64_t>(s.workers) * s.batch > (1 << 24))
+    return fail(err, errlen, BFSIM_EINVAL, "GPU path: workers*batch too large");
+  if (s.mode == BFSIM_MODE_OVERLOADED) {
+    if (s.steps < 0 || s.warmup < 0)
+      return fail(err, errlen, BFSIM_EINVAL, "run_overloaded: negative steps or warmup");
+    if (!(s.backlog >= 0.0)) return fail(err, errlen, BFSIM_EINVAL, "run_overloaded: bad backlog");
+    if (single_class_inputs && (*single_class_inputs)[s.input_id])
+      return fail(err, errlen, BFSIM_EINVAL,
+                  "run_overloaded: single-class prefill never satisfies Def. 1 (reference loops "
+                  "forever, SURVEY F12)");
+    if (s.warmup + s.steps > INT32_MAX - 2)
+      return fail(err, errlen, BFSIM_EINVAL, "run_overloaded: too many steps");
+  }
+  if (s.horizon > 4096) return fail(err, errlen, BFSIM_EINVAL, "GPU path: horizon > 4096");
+  const bfsim_input_t& in = inputs[s.input_id];
+  const int64_t d = static_cast<int64_t>(s.drift);
+  const double lb = static_cast<double>(s.batch) *
+                    (static_cast<double>(in.s_max) + static_cast<double>(d) * (in.max_decode - 1));
+  if (lb >= 2147483647.0)
+    return fail(err, errlen, BFSIM_EINVAL, "GPU path: per-worker load bound exceeds 2^31");
+  if (in.max_decode >= (1 << 30)) return fail(err, errlen, BFSIM_EINVAL, "GPU path: decode too long");
+  return BFSIM_OK;
+}
+
+int wpl_for(int G) {
+  int w = (G + 31) / 32;
+  int p = 1;
+  while (p < w) p <<= 1;
+  return p;
+}
+
+struct Group {
+  int mode, policy, wpl, small;
+  std::vector<int32_t> idx;
+  Plan plan;
+  int wpc = 4, grid = 0;
+};
+
+// Lay out every per-warp array; put the hot ones in shared memory until the
+// budget is spent, the rest in the warp's global workspace.
+void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inputs, int smem_budget) {
+  Plan& p = g.plan;
+  std::memset(&p, 0, sizeof(p));
+  int G = 1, B = 1, H = 0, S = 1, max_o = 1;
+  int64_t max_len = 0;
+  for (int32_t i : g.idx) {
+    const auto& s = scen[i];
+    const auto& in = inputs[s.input_id];
+    G = std::max(G, s.workers);
+    B = std::max(B, s.batch);
+    if (s.policy == BFSIM_POLICY_BFIO_GREEDY) H = std::max(H, s.horizon);
+    S = std::max(S, in.s_max);
+    max_o = std::max(max_o, in.max_decode);
+    max_len = std::max<int64_t>(max_len, in.length);
+  }
+  int R = 1;
+  while (R <= max_o) R <<= 1;
+  p.G = G;
+  p.B = B;
+  p.H = H;
+  p.S = S;
+  p.R = R;
+  p.umax = G * B;
+  const int wpl = g.wpl;
+  const bool greedy = g.policy == BFSIM_POLICY_BFIO_GREEDY;
+  const bool ovl = g.mode == BFSIM_MODE_OVERLOADED;
+  const int64_t GB = static_cast<int64_t>(G) * B;
+  const int rstride = (G & 1) ? G : G + 1;
+  const int64_t lvl = static_cast<int64_t>(B) + 2;
+  const int64_t bm_words = 64 + (S + 63) / 64 + 1;
+
+  struct Item {
+    int64_t* code;
+    int64_t bytes;
+  };
+  // hot first
+  std::vector<Item> items = {
+      {&p.o_rl, 32LL * rstride * 4}, {&p.o_rdt, 32 * 8}, {&p.o_rcs, 32 * 8}, {&p.o_rmx, 32 * 4},
+      {&p.o_rac, 32 * 4},            {&p.o_capb, G * 4LL}, {&p.o_asum, G * 8LL},
+      {&p.o_lvT, lvl * 4},           {&p.o_lvV, lvl * 4}, {&p.o_lvK, lvl * 4},
+      {&p.o_lvM, lvl * wpl * 4},     {&p.o_f, GB * 4},    {&p.o_stk, GB * 2},
+      {&p.o_a, GB * 4},              {&p.o_x, GB * 4},    {&p.o_id, GB * 4},
+  };
+  if (greedy || ovl) {
+    items.push_back({&p.o_cls, 4LL * (S + 2) * 4});
+    items.push_back({&p.o_bm, bm_words * 8});
+    items.push_back({&p.o_pbm, bm_words * 8});
+  }
+  if (greedy && H > 0) {
+    items.push_back({&p.o_M, (H + 1) * 8LL});
+    items.push_back({&p.o_F, (H + 1) * 8LL * G});
+    items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
+    items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
+  }
+  if (greedy) {
+    items.push_back({&p.o_res, GB * 4});
+    items.push_back({&p.o_pidx, GB * 4});
+    items.push_back({&p.o_pcl, GB * 4});
+    items.push_back({&p.o_pt, GB * 4});
+    if (H > 0) {
+      items.push_back({&p.o_oc, GB * 4});
+      items.push_back({&p.o_oo, GB * 4});
+      items.push_back({&p.o_oid, GB * 4});
+    }
+  }
+  items.push_back({&p.o_ring, R * 8LL});
+  int64_t sm_off = 0, ws_off = 0;
+  for (auto& it : items) {
+    int64_t b = (it.bytes + 15) & ~15LL;
+    if (sm_off + b <= smem_budget) {
+      *it.code = sm_off;
+      sm_off += b;
+    } else {
+      *it.code = -(ws_off + 1);
+      ws_off += b;
+    }
+  }
+  if (greedy) {  // per-class waiting deques: counting-sort layout over the input
+    int64_t b = ((max_len * 8) + 15) & ~15LL;
+    p.o_deq = -(ws_off + 1);
+    ws_off += b;
+  } else {
+    p.o_deq = -1;
+  }
+  p.smem_per_warp = static_cast<int>((sm_off + 15) & ~15LL);
+  if (p.smem_per_warp == 0) p.smem_per_warp = 16;
+  p.ws_stride = std::max<int64_t>(16, (ws_off + 255) & ~255LL);
+}
+
+int64_t est_work(const bfsim_scenario_t& s, const bfsim_input_t& in) {
+  if (s.mode == BFSIM_MODE_OVERLOADED) return (s.steps + s.warmup) * s.workers;
+  return in.length * 64 + 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bfsim_ctx_create(int device, bfsim_ctx_t** out, char* err, size_t errlen) {
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(err, errlen, BFSIM_ECUDA, "no CUDA device: the GPU path has no CPU fallback");
+  if (device < 0 || device >= n) return fail(err, errlen, BFSIM_EINVAL, "device out of range");
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(err, errlen, e, "cudaSetDevice");
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10)
+    return fail(err, errlen, BFSIM_ECUDA, "the step engine is built for sm_100a (B200)");
+  auto* c = new bfsim_ctx;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  c->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+  for (int i = 0; i < kMaxGroups; ++i) {
+    cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  cudaEventCreate(&c->t0);
+  cudaEventCreate(&c->t1);
+  *out = c;
+  return BFSIM_OK;
+}
+
+void bfsim_ctx_destroy(bfsim_ctx_t* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  DevBuf* bufs[] = {&c->scen,  &c->inputs, &c->cbase, &c->traces, &c->streams, &c->results,
+                    &c->st_cs, &c->st_dt,  &c->st_mx, &c->st_ac,  &c->st_ld,   &c->rq_as,
+                    &c->rq_ss, &c->rq_wk,  &c->rq_ac, &c->rq_fc,  &c->order,   &c->ws,
+                    &c->queue};
+  for (auto* b : bufs) b->release();
+  for (int i = 0; i < kMaxGroups; ++i) {
+    cudaStreamDestroy(c->side[i]);
+    cudaEventDestroy(c->join[i]);
+  }
+  cudaEventDestroy(c->fork);
+  cudaEventDestroy(c->t0);
+  cudaEventDestroy(c->t1);
+  delete c;
+}
+
+int bfsim_ctx_device(const bfsim_ctx_t* c) { return c ? c->device : -1; }
+
+int64_t bfsim_last_launch_count(const bfsim_ctx_t* c) { return c ? c->last_launches : 0; }
+
+double bfsim_last_step_kernel_ms(const bfsim_ctx_t* c) {
+  if (!c || !c->timed) return 0.0;
+  float ms = 0.f;
+  if (cudaEventSynchronize(c->t1) != cudaSuccess) return 0.0;
+  if (cudaEventElapsedTime(&ms, c->t0, c->t1) != cudaSuccess) return 0.0;
+  return static_cast<double>(ms);
+}
+
+int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, int64_t n_scen,
+                           const bfsim_input_t* inputs_host, int32_t n_inputs,
+                           const int32_t* class_base_dev, const bfsim_request_t* traces_dev,
+                           const bfsim_sample_t* streams_dev, const bfsim_step_sink_t* steps_dev,
+                           const bfsim_req_sink_t* reqs_dev, bfsim_result_t* results_dev,
+                           void* stream, char* err, size_t errlen) {
+  if (!ctx) return fail(err, errlen, BFSIM_EINVAL, "null context");
+  ctx->last_launches = 0;
+  ctx->timed = false;
+  if (n_scen <= 0) return BFSIM_OK;
+  if (n_scen > INT32_MAX) return fail(err, errlen, BFSIM_EINVAL, "too many scenarios");
+  cudaSetDevice(ctx->device);
+  // scenarios must refer to device-resident scenario rows for the kernel: copy
+  cudaStream_t us = static_cast<cudaStream_t>(stream);
+  for (int64_t i = 0; i < n_scen; ++i) {
+    int rc = validate_scenario(scen_host[i], inputs_host, n_inputs, nullptr, err, errlen);
+    if (rc) {
+      std::string m = "scenario " + std::to_string(i) + ": " + (err ? std::string(err) : "");
+      return fail(err, errlen, rc, m.c_str());
+    }
+    const auto& in = inputs_host[scen_host[i].input_id];
+    if (scen_host[i].mode == BFSIM_MODE_POISSON && !traces_dev && in.length > 0)
+      return fail(err, errlen, BFSIM_EINVAL, "poisson scenario without traces");
+    if (scen_host[i].mode == BFSIM_MODE_OVERLOADED && !streams_dev)
+      return fail(err, errlen, BFSIM_EINVAL, "overloaded scenario without sample streams");
+  }
+  // group by kernel variant; LPT order inside a group
+  std::map<std::tuple<int, int, int, int>, Group> groups;
+  for (int64_t i = 0; i < n_scen; ++i) {
+    const auto& s = scen_host[i];
+    const auto& in = inputs_host[s.input_id];
+    int small = in.s_max <= 64 ? 1 : 0;
+    int wpl = wpl_for(s.workers);
+    auto key = std::make_tuple(s.mode, s.policy, wpl, small);
+    auto& g = groups[key];
+    g.mode = s.mode;
+    g.policy = s.policy;
+    g.wpl = wpl;
+    g.small = small;
+    g.idx.push_back(static_cast<int32_t>(i));
+  }
+  if (static_cast<int>(groups.size()) > kMaxGroups)
+    return fail(err, errlen, BFSIM_EINVAL, "too many distinct kernel variants in one batch");
+  std::vector<int32_t> order;
+  std::vector<Group*> gl;
+  int64_t ws_total = 0;
+  for (auto& kv : groups) {
+    Group& g = kv.second;
+    std::stable_sort(g.idx.begin(), g.idx.end(), [&](int32_t a, int32_t b) {
+      return est_work(scen_host[a], inputs_host[scen_host[a].input_id]) >
+             est_work(scen_host[b], inputs_host[scen_host[b].input_id]);
+    });
+    // shared memory: up to 4 warps per CTA within the opt-in limit
+    int budget = std::min(ctx->smem_optin / 4 - 64, 200 * 1024);
+    make_plan(g, scen_host, inputs_host, budget);
+    g.wpc = std::max(1, std::min(4, ctx->smem_optin / std::max(1, g.plan.smem_per_warp)));
+    KParams probe{};
+    probe.plan = g.plan;
+    int occ = 0;
+    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, probe, 0, g.wpc, nullptr,
+                                       &occ);
+    if (rc != 0 || occ <= 0)
+      return fail(err, errlen, BFSIM_ECUDA, "step kernel does not fit on the device");
+    int64_t warps_needed = static_cast<int64_t>(g.idx.size());
+    int64_t ctas = (warps_needed + g.wpc - 1) / g.wpc;
+    g.grid = static_cast<int>(std::min<int64_t>(ctas, static_cast<int64_t>(occ) * ctx->sm_count));
+    ws_total += g.plan.ws_stride * g.grid * g.wpc;
+    gl.push_back(&g);
+  }
+  for (auto* g : gl) order.insert(order.end(), g->idx.begin(), g->idx.end());
+  cudaError_t e;
+  if ((e = ctx->order.ensure(order.size() * 4)) != cudaSuccess) return cuda_fail(err, errlen, e, "alloc");
+  if ((e = ctx->queue.ensure(kMaxGroups * 4)) != cudaSuccess) return cuda_fail(err, errlen, e, "alloc");
+  if ((e = ctx->ws.ensure(static_cast<size_t>(std::max<int64_t>(ws_total, 256)))) != cudaSuccess)
+    return cuda_fail(err, errlen, e, "workspace alloc");
+  // device copy of the scenario table (the host table is authoritative)
+  if ((e = ctx->scen.ensure(n_scen * sizeof(bfsim_scenario_t))) != cudaSuccess)
+    return cuda_fail(err, errlen, e, "alloc");
+  if ((e = ctx->inputs.ensure(n_inputs * sizeof(bfsim_input_t))) != cudaSuccess)
+    return cuda_fail(err, errlen, e, "alloc");
+  cudaMemcpyAsync(ctx->scen.p, scen_host, n_scen * sizeof(bfsim_scenario_t), cudaMemcpyHostToDevice, us);
+  cudaMemcpyAsync(ctx->inputs.p, inputs_host, n_inputs * sizeof(bfsim_input_t), cudaMemcpyHostToDevice, us);
+  cudaMemcpyAsync(ctx->order.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice, us);
+  cudaMemsetAsync(ctx->queue.p, 0, kMaxGroups * 4, us);
+  int64_t launches = 0;  // counted below: kernels only (not copies / memsets)
+  cudaEventRecord(ctx->t0, us);
+  cudaEventRecord(ctx->fork, us);
+  int64_t off = 0, ws_off = 0;
+  for (size_t gi = 0; gi < gl.size(); ++gi) {
+    Group& g = *gl[gi];
+    cudaStream_t s = gl.size() == 1 ? us : ctx->side[gi];
+    if (gl.size() > 1) cudaStreamWaitEvent(s, ctx->fork, 0);
+    KParams kp{};
+    kp.scen = static_cast<const bfsim_scenario_t*>(ctx->scen.p);
+    kp.order = static_cast<const int32_t*>(ctx->order.p) + off;
+    kp.n = static_cast<int32_t>(g.idx.size());
+    kp.inputs = static_cast<const bfsim_input_t*>(ctx->inputs.p);
+    kp.class_base = class_base_dev;
+    kp.traces = traces_dev;
+    kp.streams = streams_dev;
+    if (steps_dev) kp.steps = *steps_dev;
+    if (reqs_dev) kp.reqs = *reqs_dev;
+    kp.results = results_dev;
+    kp.ws = static_cast<unsigned char*>(ctx->ws.p) + ws_off;
+    kp.queue = static_cast<int32_t*>(ctx->queue.p) + gi;
+    kp.plan = g.plan;
+    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, kp, g.grid, g.wpc, s, nullptr);
+    if (rc != 0) return cuda_fail(err, errlen, static_cast<cudaError_t>(rc), "step kernel launch");
+    ++launches;
+    if (gl.size() > 1) {
+      cudaEventRecord(ctx->join[gi], s);
+      cudaStreamWaitEvent(us, ctx->join[gi], 0);
+    }
+    off += static_cast<int64_t>(g.idx.size());
+    ws_off += g.plan.ws_stride * g.grid * g.wpc;
+  }
+  cudaEventRecord(ctx->t1, us);
+  ctx->timed = true;
+  ctx->last_launches = launches;
+  return BFSIM_OK;
+}
+
+int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_scen,
+                    const bfsim_input_t* inputs, int32_t n_inputs, const int32_t* class_base,
+                    int64_t n_class_base, const bfsim_request_t* traces, int64_t n_trace_records,
+                    const bfsim_sample_t* streams, int64_t n_stream_samples,
+                    const bfsim_step_sink_t* steps, int64_t n_step_records, int64_t n_load_values,
+                    const bfsim_req_sink_t* reqs, int64_t n_req_entries, bfsim_result_t* results,
+                    char* err, size_t errlen) {
+  if (!ctx) return fail(err, errlen, BFSIM_EINVAL, "null context");
+  cudaSetDevice(ctx->device);
+  // host-side validation that needs the host inputs (single-class streams, bounds)
+  std::vector<int> single(static_cast<size_t>(n_inputs), 0);
+  for (int32_t i = 0; i < n_inputs; ++i) {
+    const auto& in = inputs[i];
+    if (in.offset < 0 || in.length < 0)
+      return fail(err, errlen, BFSIM_EINVAL, "input: negative offset/length");
+    if (in.class_base_offset < 0 || in.class_base_offset + in.s_max + 2 > n_class_base)
+      return fail(err, errlen, BFSIM_EINVAL, "input: class_base slice out of range");
+  }
+  for (int64_t i = 0; i < n_scen; ++i) {
+    const auto& s = scen[i];
+    if (s.input_id < 0 || s.input_id >= n_inputs)
+      return fail(err, errlen, BFSIM_EINVAL, "scenario: input_id out of range");
+    const auto& in = inputs[s.input_id];
+    if (s.mode == BFSIM_MODE_OVERLOADED) {
+      if (in.offset + in.length > n_stream_samples)
+        return fail(err, errlen, BFSIM_EINVAL, "input: stream slice out of range");
+      bool one = true;
+      for (int64_t j = 1; j < in.length && one; ++j)
+        one = streams[in.offset + j].prefill == streams[in.offset].prefill;
+      single[s.input_id] = one ? 1 : 0;
+    } else if (in.offset + in.length > n_trace_records) {
+      return fail(err, errlen, BFSIM_EINVAL, "input: trace slice out of range");
+    }
+    if (steps && steps->clock_start && s.step_capacity > 0 &&
+        (s.step_offset < 0 || s.step_offset + s.step_capacity > n_step_records ||
+         s.load_offset < 0 || s.load_offset + s.step_capacity * s.workers > n_load_values))
+      return fail(err, errlen, BFSIM_EINVAL, "scenario: step sink slice out of range");
+    if (reqs && reqs->start_step &&
+        (s.req_offset < 0 || s.req_offset + in.length > n_req_entries))
+      return fail(err, errlen, BFSIM_EINVAL, "scenario: request sink slice out of range");
+    int rc = validate_scenario(s, inputs, n_inputs, &single, err, errlen);
+    if (rc) {
+      std::string m = "scenario " + std::to_string(i) + ": " + (err ? std::string(err) : "");
+      return fail(err, errlen, rc, m.c_str());
+    }
+  }
+  cudaError_t e;
+  cudaStream_t us = nullptr;
+  auto up = [&](DevBuf& b, const void* h, size_t bytes) -> cudaError_t {
+    cudaError_t x = b.ensure(std::max<size_t>(bytes, 16));
+    if (x != cudaSuccess) return x;
+    if (bytes) x = cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, us);
+    return x;
+  };
+  if ((e = up(ctx->cbase, class_base, n_class_base * 4)) != cudaSuccess) return cuda_fail(err, errlen, e, "H2D");
+  if (traces && n_trace_records)
+    if ((e = up(ctx->traces, traces, n_trace_records * sizeof(bfsim_request_t))) != cudaSuccess)
+      return cuda_fail(err, errlen, e, "H2D");
+  if (streams && n_stream_samples)
+    if ((e = up(ctx->streams, streams, n_stream_samples * sizeof(bfsim_sample_t))) != cudaSuccess)
+      return cuda_fail(err, errlen, e, "H2D");
+  if ((e = ctx->results.ensure(n_scen * sizeof(bfsim_result_t))) != cudaSuccess)
+    return cuda_fail(err, errlen, e, "alloc");
+  bfsim_step_sink_t dsteps{};
+  bool want_steps = steps && steps->clock_start && n_step_records > 0;
+  if (want_steps) {
+    if ((e = ctx->st_cs.ensure(n_step_records * 8)) || (e = ctx->st_dt.ensure(n_step_records * 8)) ||
+        (e = ctx->st_mx.ensure(n_step_records * 8)) || (e = ctx->st_ac.ensure(n_step_records * 8)) ||
+        (e = ctx->st_ld.ensure(std::max<int64_t>(n_load_values, 1) * 8)))
+      return cuda_fail(err, errlen, e, "alloc");
+    dsteps.clock_start = static_cast<double*>(ctx->st_cs.p);
+    dsteps.dt = static_cast<double*>(ctx->st_dt.p);
+    dsteps.max_load = static_cast<double*>(ctx->st_mx.p);
+    dsteps.active_count = static_cast<int64_t*>(ctx->st_ac.p);
+    dsteps.loads = static_cast<double*>(ctx->st_ld.p);
+  }
+  bfsim_req_sink_t dreqs{};
+  bool want_reqs = reqs && reqs->start_step && n_req_entries > 0;
+  if (want_reqs) {
+    if ((e = ctx->rq_as.ensure(n_req_entries * 4)) || (e = ctx->rq_ss.ensure(n_req_entries * 4)) ||
+        (e = ctx->rq_wk.ensure(n_req_entries * 4)) || (e = ctx->rq_ac.ensure(n_req_entries * 8)) ||
+        (e = ctx->rq_fc.ensure(n_req_entries * 8)))
+      return cuda_fail(err, errlen, e, "alloc");
+    dreqs.arrival_step = static_cast<int32_t*>(ctx->rq_as.p);
+    dreqs.start_step = static_cast<int32_t*>(ctx->rq_ss.p);
+    dreqs.worker = static_cast<int32_t*>(ctx->rq_wk.p);
+    dreqs.admit_clock = static_cast<double*>(ctx->rq_ac.p);
+    dreqs.finish_clock = static_cast<double*>(ctx->rq_fc.p);
+  }
+  int rc = bfsim_run_batch_device(
+      ctx, scen, n_scen, inputs, n_inputs, static_cast<const int32_t*>(ctx->cbase.p),
+      traces ? static_cast<const bfsim_request_t*>(ctx->traces.p) : nullptr,
+      streams ? static_cast<const bfsim_sample_t*>(ctx->streams.p) : nullptr,
+      want_steps ? &dsteps : nullptr, want_reqs ? &dreqs : nullptr,
+      static_cast<bfsim_result_t*>(ctx->results.p), us, err, errlen);
+  if (rc) return rc;
+  auto down = [&](void* h, const DevBuf& b, size_t bytes) {
+    if (h && bytes) cudaMemcpyAsync(h, b.p, bytes, cudaMemcpyDeviceToHost, us);
+  };
+  down(results, ctx->results, n_scen * sizeof(bfsim_result_t));
+  if (want_steps) {
+    down(steps->clock_start, ctx->st_cs, n_step_records * 8);
+    down(steps->dt, ctx->st_dt, n_step_records * 8);
+    down(steps->max_load, ctx->st_mx, n_step_records * 8);
+    down(steps->active_count, ctx->st_ac, n_step_records * 8);
+    down(steps->loads, ctx->st_ld, n_load_values * 8);
+  }
+  if (want_reqs) {
+    down(reqs->arrival_step, ctx->rq_as, n_req_entries * 4);
+    down(reqs->start_step, ctx->rq_ss, n_req_entries * 4);
+    down(reqs->worker, ctx->rq_wk, n_req_entries * 4);
+    down(reqs->admit_clock, ctx->rq_ac, n_req_entries * 8);
+    down(reqs->finish_clock, ctx->rq_fc, n_req_entries * 8);
+  }
+  if ((e = cudaStreamSynchronize(us)) != cudaSuccess) return cuda_fail(err, errlen, e, "step kernel");
+  int first = BFSIM_OK;
+  for (int64_t i = 0; i < n_scen; ++i) {
+    int st = results[i].status;
+    if (st != BFSIM_OK && st != BFSIM_PARTIAL && first == BFSIM_OK) first = st;
+  }
+  if (first == BFSIM_ESTREAM)
+    return fail(err, errlen, BFSIM_ESTREAM, "overloaded sample stream exhausted");
+  return first;
+}
+
+}  // extern "C"

@@ -1,0 +1,1126 @@
+#pragma once
+// B200 (sm_100a) batched step engine for the BF-IO hot path.
+//
+// One warp simulates one trajectory (scenario) end to end; persistent warps
+// pull scenarios from an atomic queue. Worker g is owned by lane g % 32 (slot
+// j = g / 32 of WPL register-resident workers per lane), so per-worker state
+// (active count, load aggregate) lives in registers and every per-worker
+// update is lane-local. Per-slot, per-class and lookahead-window state lives in
+// the warp's shared-memory arena; the per-prefill-class waiting deques live in
+// a per-warp global workspace (L2-resident).
+//
+// Reference semantics (paths under /root/reference/proj/include/bfsim/):
+//   step order            engine.hpp:112-160 (Poisson), oracle.hpp:163-242 (overloaded)
+//   reveal                engine.hpp:123-128
+//   fcfs / jsq            policies.hpp:100-138   -> closed-form level filling
+//   bfio-greedy           policies.hpp:269-370   -> class-deque water filling (F4)
+//                                                   + warp-argmin placement (F3)
+//   loads / dt / clock    engine.hpp:136-146 (dt = C (+) t (x) max, no FMA: F6)
+//   completion            engine.hpp:149-157, 118-120; oracle.hpp:225-240
+//   accounting            metrics.hpp:17-126, metrics_power.hpp:24-27
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "engine.cuh"
+
+// Template implementation of the step kernel; instantiated per (mode, policy)
+// in engine_<mode>_<policy>.cu so the variants compile in parallel.
+
+namespace bfsim {
+namespace detail {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint64_t wmin_u64(uint64_t v) {
+  uint32_t hi = __reduce_min_sync(FULLMASK, static_cast<uint32_t>(v >> 32));
+  uint32_t lo = __reduce_min_sync(
+      FULLMASK, static_cast<uint32_t>(v >> 32) == hi ? static_cast<uint32_t>(v) : 0xFFFFFFFFu);
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+__device__ __forceinline__ long long wsum_i64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double wsum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULLMASK, v, o));
+  return v;
+}
+
+// Array placement code from the planner: >= 0 is a byte offset into the warp's
+// shared-memory arena, < 0 encodes (-code - 1) bytes into its global workspace.
+template <class T>
+__device__ __forceinline__ T* at(unsigned char* sm, unsigned char* ws, int64_t code) {
+  return code >= 0 ? reinterpret_cast<T*>(sm + code) : reinterpret_cast<T*>(ws + (-code - 1));
+}
+
+__device__ __forceinline__ int bits_for(long long x) {  // bits to hold values 0..x
+  return x <= 0 ? 0 : 64 - __clzll(static_cast<unsigned long long>(x));
+}
+
+// ---------------------------------------------------------------------------
+// Set of non-empty prefill classes c = 1..S (bit c-1). SMALL: S <= 64 in one
+// register word. Otherwise a 3-level 64-ary bitmap (top word in a register,
+// mid/leaf words in shared or global memory). All lanes execute every
+// operation uniformly; lane 0 performs the stores.
+template <bool SMALL>
+struct ClassSet;
+
+template <>
+struct ClassSet<true> {
+  uint64_t bits;
+  __device__ void init(uint64_t*, uint64_t*, int) { bits = 0; }
+  __device__ bool empty() const { return bits == 0; }
+  __device__ int highest() const { return bits ? 64 - __clzll(bits) : 0; }
+  __device__ int lowest() const { return bits ? __ffsll(static_cast<long long>(bits)) : 0; }
+  __device__ int highest_le(long long d) const {
+    if (d < 1) return 0;
+    uint64_t m = d >= 64 ? bits : (bits & ((1ull << d) - 1ull));
+    return m ? 64 - __clzll(m) : 0;
+  }
+  __device__ void clear(int c) { bits &= ~(1ull << (c - 1)); }
+  // lanes with `has` contribute class c; result is uniform
+  __device__ void add_from_lanes(bool has, int c) {
+    uint64_t m = has ? (1ull << (c - 1)) : 0ull;
+    uint32_t lo = __reduce_or_sync(FULLMASK, static_cast<uint32_t>(m));
+    uint32_t hi = __reduce_or_sync(FULLMASK, static_cast<uint32_t>(m >> 32));
+    bits |= (static_cast<uint64_t>(hi) << 32) | lo;
+  }
+  __device__ void add_uniform(int c) { bits |= 1ull << (c - 1); }
+};
+
+template <>
+struct ClassSet<false> {
+  uint64_t top;    // bit m: mid word m non-empty
+  uint64_t* mid;   // 64 words; bit w: leaf word w non-empty
+  uint64_t* leaf;  // ceil(S/64) words; bit b: class b+1 present
+  int nbits;       // S
+  __device__ void init(uint64_t* mid_, uint64_t* leaf_, int S) {
+    mid = mid_;
+    leaf = leaf_;
+    nbits = S;
+    top = 0;
+    const int lane = threadIdx.x & 31;
+    int nl = (S + 63) >> 6;
+    for (int i = lane; i < nl; i += 32) leaf[i] = 0;
+    for (int i = lane; i < 64; i += 32) mid[i] = 0;
+    __syncwarp();
+  }
+  __device__ bool empty() const { return top == 0; }
+  __device__ static uint64_t mask_le(int b) {  // bits 0..b
+    return b >= 63 ? ~0ull : ((1ull << (b + 1)) - 1ull);
+  }
+  __device__ int from_top(uint64_t m2) const {  // highest class under top mask m2
+    int mw = 63 - __clzll(m2);
+    int lw = (mw << 6) + 63 - __clzll(mid[mw]);
+    return (lw << 6) + 63 - __clzll(leaf[lw]) + 1;
+  }
+  __device__ int highest() const { return top ? from_top(top) : 0; }
+  __device__ int lowest() const {
+    if (!top) return 0;
+    int mw = __ffsll(static_cast<long long>(top)) - 1;
+    int lw = (mw << 6) + __ffsll(static_cast<long long>(mid[mw])) - 1;
+    return (lw << 6) + __ffsll(static_cast<long long>(leaf[lw]));
+  }
+  // largest class c <= d, 0 if none
+  __device__ int highest_le(long long d) const {
+    if (d < 1 || !top) return 0;
+    long long q = d - 1;
+    if (q > nbits - 1) q = nbits - 1;
+    const int w0 = static_cast<int>(q >> 6);
+    const int mw0 = w0 >> 6;
+    if ((top >> mw0) & 1ull) {
+      uint64_t lm = leaf[w0] & mask_le(static_cast<int>(q & 63));
+      if (lm) return (w0 << 6) + 63 - __clzll(lm) + 1;
+      if (w0 & 63) {
+        uint64_t mm = mid[mw0] & mask_le((w0 & 63) - 1);
+        if (mm) {
+          int lw = (mw0 << 6) + 63 - __clzll(mm);
+          return (lw << 6) + 63 - __clzll(leaf[lw]) + 1;
+        }
+      }
+    }
+    if (mw0 == 0) return 0;
+    uint64_t tm = top & mask_le(mw0 - 1);
+    return tm ? from_top(tm) : 0;
+  }
+  __device__ void clear(int c) {
+    const int lane = threadIdx.x & 31;
+    int b = c - 1, w = b >> 6;
+    uint64_t lw = leaf[w] & ~(1ull << (b & 63));
+    uint64_t m2 = mid[w >> 6] & ~(1ull << (w & 63));
+    __syncwarp();
+    if (lane == 0) leaf[w] = lw;
+    if (lw == 0) {
+      if (lane == 0) mid[w >> 6] = m2;
+      if (m2 == 0) top &= ~(1ull << (w >> 6));
+    }
+    __syncwarp();
+  }
+  __device__ void add_from_lanes(bool has, int c) {
+    uint64_t tb = 0;
+    if (has) {
+      int b = c - 1, w = b >> 6;
+      atomicOr(reinterpret_cast<unsigned long long*>(&leaf[w]), 1ull << (b & 63));
+      atomicOr(reinterpret_cast<unsigned long long*>(&mid[w >> 6]), 1ull << (w & 63));
+      tb = 1ull << (w >> 6);
+    }
+    uint32_t lo = __reduce_or_sync(FULLMASK, static_cast<uint32_t>(tb));
+    uint32_t hi = __reduce_or_sync(FULLMASK, static_cast<uint32_t>(tb >> 32));
+    top |= (static_cast<uint64_t>(hi) << 32) | lo;
+    __syncwarp();
+  }
+  __device__ void add_uniform(int c) {
+    const int lane = threadIdx.x & 31;
+    int b = c - 1, w = b >> 6;
+    __syncwarp();
+    if (lane == 0) {
+      leaf[w] |= 1ull << (b & 63);
+      mid[w >> 6] |= 1ull << (w & 63);
+    }
+    top |= 1ull << (w >> 6);
+    __syncwarp();
+  }
+};
+
+// ---------------------------------------------------------------------------
+
+template <int MODE, int POL, int WPL, bool SMALLC>
+__device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned char* ws) {
+  constexpr bool OVL = MODE == BFSIM_MODE_OVERLOADED;
+  constexpr bool GREEDY = POL == BFSIM_POLICY_BFIO_GREEDY;
+  constexpr bool JSQ = POL == BFSIM_POLICY_JSQ;
+  const Plan& pl = P.plan;
+  const int lane = threadIdx.x & 31;
+  const bfsim_scenario_t sc = P.scen[si];
+  const bfsim_input_t in = P.inputs[sc.input_id];
+  const int G = sc.workers, B = sc.batch;
+  const int H = GREEDY ? sc.horizon : 0;
+  const int Hm = H > 0 ? H : 1;  // modulus for the window ring (unused when H == 0)
+  const bool trunc = sc.lookahead == BFSIM_LOOKAHEAD_TRUNCATED;
+  const long long d = static_cast<long long>(sc.drift);
+  const int S = in.s_max;
+  const long long N = in.length;
+  const bfsim_request_t* tr = P.traces ? P.traces + in.offset : nullptr;
+  const bfsim_sample_t* st = P.streams ? P.streams + in.offset : nullptr;
+  const int32_t* cbase = P.class_base + in.class_base_offset;
+  const double C0 = sc.overhead, TL = sc.per_token;
+  const double p_idle = sc.p_idle, p_diff = sc.p_max - sc.p_idle, gam = sc.gamma;
+  const long long warmup = OVL ? sc.warmup : 0;
+  const long long total_steps =
+      OVL ? sc.warmup + sc.steps : (sc.max_steps < INT_MAX - 2 ? sc.max_steps : INT_MAX - 2);
+  const bool emit_steps = P.steps.clock_start != nullptr;
+  const bool emit_reqs = P.reqs.start_step != nullptr;
+  const long long so = sc.step_offset, scap = sc.step_capacity, lo = sc.load_offset;
+  const long long ro = sc.req_offset;
+  const int rstride = (G & 1) ? G : G + 1;  // padded accounting-ring row (bank conflicts)
+
+  // --- arenas (shared memory, or the warp's global workspace when too big) --
+  uint32_t* s_f = at<uint32_t>(sm, ws, pl.o_f);
+  int32_t* s_a = at<int32_t>(sm, ws, pl.o_a);
+  int32_t* s_x = at<int32_t>(sm, ws, pl.o_x);
+  int32_t* s_id = at<int32_t>(sm, ws, pl.o_id);
+  uint16_t* s_stk = at<uint16_t>(sm, ws, pl.o_stk);
+  int32_t* s_capb = at<int32_t>(sm, ws, pl.o_capb);
+  unsigned long long* s_asum = at<unsigned long long>(sm, ws, pl.o_asum);
+  uint32_t* r_l = at<uint32_t>(sm, ws, pl.o_rl);
+  double* r_dt = at<double>(sm, ws, pl.o_rdt);
+  double* r_cs = at<double>(sm, ws, pl.o_rcs);
+  uint32_t* r_mx = at<uint32_t>(sm, ws, pl.o_rmx);
+  int32_t* r_ac = at<int32_t>(sm, ws, pl.o_rac);
+  double* ring = at<double>(sm, ws, pl.o_ring);
+  const int Rm = pl.R - 1;
+  int32_t* c_front = at<int32_t>(sm, ws, pl.o_cls);
+  int32_t* c_back = c_front + (pl.S + 2);
+  int32_t* c_pc = c_back + (pl.S + 2);
+  int32_t* c_cs = c_pc + (pl.S + 2);
+  int2* deq = at<int2>(sm, ws, pl.o_deq);
+  int32_t* p_idx = at<int32_t>(sm, ws, pl.o_pidx);
+  int32_t* p_cl = at<int32_t>(sm, ws, pl.o_pcl);
+  int32_t* p_t = at<int32_t>(sm, ws, pl.o_pt);
+  uint32_t* s_res = at<uint32_t>(sm, ws, pl.o_res);
+  int32_t* lvT = at<int32_t>(sm, ws, pl.o_lvT);
+  int32_t* lvV = at<int32_t>(sm, ws, pl.o_lvV);
+  int32_t* lvK = at<int32_t>(sm, ws, pl.o_lvK);
+  uint32_t* lvM = at<uint32_t>(sm, ws, pl.o_lvM);
+  long long* s_F = at<long long>(sm, ws, pl.o_F);
+  long long* s_M = at<long long>(sm, ws, pl.o_M);
+  int32_t* s_Wc = at<int32_t>(sm, ws, pl.o_Wc);
+  long long* s_Wa = at<long long>(sm, ws, pl.o_Wa);
+  int32_t* o_c = at<int32_t>(sm, ws, pl.o_oc);
+  int32_t* o_o = at<int32_t>(sm, ws, pl.o_oo);
+  int32_t* o_id = at<int32_t>(sm, ws, pl.o_oid);
+
+  // --- init ----------------------------------------------------------------
+  for (int i = lane; i < G * B; i += 32) {
+    s_f[i] = kEmpty;
+    s_stk[i] = static_cast<uint16_t>(i % B);
+  }
+  const bool use_classes = GREEDY || OVL;
+  if (use_classes)
+    for (int c = lane; c <= S + 1; c += 32) {
+      c_front[c] = 0;
+      c_back[c] = 0;
+      c_pc[c] = 0;
+    }
+  if (GREEDY && H > 0)
+    for (int i = lane; i < H * G; i += 32) {
+      s_Wc[i] = 0;
+      s_Wa[i] = 0;
+    }
+  for (int i = lane; i < G; i += 32) s_asum[i] = 0;
+  ClassSet<SMALLC> wset, pset;  // waiting classes; classes picked in phase 1
+  {
+    uint64_t* bm = at<uint64_t>(sm, ws, pl.o_bm);
+    uint64_t* pbm = at<uint64_t>(sm, ws, pl.o_pbm);
+    wset.init(bm, bm + 64, S);
+    pset.init(pbm, pbm + 64, S);
+  }
+  __syncwarp();
+
+  int n[WPL];
+  long long A[WPL];
+#pragma unroll
+  for (int j = 0; j < WPL; ++j) {
+    n[j] = 0;
+    A[j] = 0;
+  }
+  const int gbits = bits_for(G - 1) > 0 ? bits_for(G - 1) : 1;
+  const uint64_t gmask = (1ull << gbits) - 1ull;
+  // largest per-worker load: B requests at their largest workload
+  const long long lbound =
+      static_cast<long long>(B) * (static_cast<long long>(S) + d * (in.max_decode - 1));
+  const bool k32 = bits_for(lbound) + gbits <= 31;
+
+  long long k = 0;
+  double clock = 0.0;
+  long long nxt = 0, head = 0, n_wait = 0, act = 0, done = 0, tail = 0, adm_total = 0;
+  long long maxcount = 0;
+  const long long min_pool =
+      OVL ? static_cast<long long>(sc.backlog * static_cast<double>(G) * static_cast<double>(B)) : 0;
+  long long imb = 0, work = 0, tok = 0, records = 0;
+  double energy = 0.0, elapsed = 0.0, tpot_sum = 0.0;
+  int status = BFSIM_OK;
+  uint32_t flags = 0;
+
+  // reveal window: lane j holds trace record nxt + j
+  double w_arr = 0.0;
+  int w_s = 0, w_o = 0;
+  auto load_rec = [&](long long idx) {
+    if (idx < N) {
+      int4 v = __ldg(reinterpret_cast<const int4*>(tr) + idx);
+      w_arr = __hiloint2double(v.y, v.x);
+      w_s = v.z;
+      w_o = v.w;
+    }
+  };
+  if (!OVL) load_rec(lane);
+
+  // ---- per-step accounting flush: steps k0 .. k0+cnt-1 in ring rows 0..cnt-1
+  auto flush = [&](long long k0, int cnt) {
+    double dp = 0.0, dtl = 0.0;
+    long long imb_l = 0, sum_l = 0, ac_l = 0;
+    bool counted = false;
+    if (lane < cnt) {
+      long long kk = k0 + lane;
+      counted = kk >= warmup;
+      uint32_t mx = r_mx[lane];
+      double dt = r_dt[lane];
+      const uint32_t* row = r_l + lane * rstride;
+      double mxd = static_cast<double>(mx);
+      double p = 0.0;
+      unsigned long long smv = 0;
+      for (int g = 0; g < G; ++g) {
+        uint32_t L = row[g];
+        smv += L;
+        // utilization u = L / max (metrics.hpp:56-62), power (metrics_power.hpp:24-27)
+        double u = mx ? __ddiv_rn(static_cast<double>(L), mxd) : 0.0;
+        p = __dadd_rn(p, __dadd_rn(p_idle, __dmul_rn(p_diff, pow(u, gam))));
+      }
+      if (counted) {
+        imb_l = static_cast<long long>(G) * mx - static_cast<long long>(smv);
+        sum_l = static_cast<long long>(smv);
+        ac_l = r_ac[lane];
+        dp = __dmul_rn(dt, p);
+        dtl = dt;
+      }
+      if (emit_steps && kk < scap) {
+        P.steps.clock_start[so + kk] = r_cs[lane];
+        P.steps.dt[so + kk] = dt;
+        P.steps.max_load[so + kk] = mxd;
+        P.steps.active_count[so + kk] = r_ac[lane];
+      }
+    }
+    imb += wsum_i64(imb_l);
+    work += wsum_i64(sum_l);
+    tok += wsum_i64(ac_l);
+    unsigned cm = __ballot_sync(FULLMASK, counted);
+    records += __popc(cm);
+    // energy and elapsed summed in step order, as metrics.hpp:32-40,67-76
+    for (int i = 0; i < cnt; ++i) {
+      double e = __shfl_sync(FULLMASK, dp, i);
+      double t = __shfl_sync(FULLMASK, dtl, i);
+      if ((cm >> i) & 1u) {
+        energy = __dadd_rn(energy, e);
+        elapsed = __dadd_rn(elapsed, t);
+      }
+    }
+    if (emit_steps && k0 < scap) {
+      long long rows = scap - k0 < cnt ? scap - k0 : cnt;
+      for (long long r = 0; r < rows; ++r)
+        for (int g = lane; g < G; g += 32)
+          P.steps.loads[lo + (k0 + r) * G + g] = static_cast<double>(r_l[r * rstride + g]);
+    }
+    __syncwarp();
+  };
+
+  // ---- Poisson reveal (engine.hpp:123-128) ----
+  auto reveal = [&]() {
+    for (;;) {
+      bool ok = (nxt + lane < N) && (w_arr <= clock);
+      unsigned m = __ballot_sync(FULLMASK, ok);
+      int cnt = __popc(m);  // arrivals sorted: m is a prefix of the lanes
+      if (cnt == 0) break;
+      long long id = nxt + lane;
+      if (ok && emit_reqs) {
+        P.reqs.arrival_step[ro + id] = static_cast<int32_t>(k);
+        P.reqs.start_step[ro + id] = -1;
+        P.reqs.worker[ro + id] = -1;
+        P.reqs.admit_clock[ro + id] = 0.0;
+        P.reqs.finish_clock[ro + id] = 0.0;
+      }
+      if constexpr (GREEDY) {
+        // push to the back of the per-class deque, arrival order within class
+        int pos = 0, npeer = 0;
+        bool leader = false;
+        if (ok) {
+          unsigned peers = __match_any_sync(m, w_s);
+          pos = c_back[w_s] + __popc(peers & lanemask_lt());
+          npeer = __popc(peers);
+          leader = (__ffs(peers) - 1) == lane;
+        }
+        __syncwarp();
+        if (ok) {
+          deq[cbase[w_s] + pos] = make_int2(static_cast<int>(id), w_o);
+          if (leader) c_back[w_s] = pos + npeer;
+        }
+        wset.add_from_lanes(ok, ok ? w_s : 1);
+        __syncwarp();
+      }
+      n_wait += cnt;
+      nxt += cnt;
+      // shift the window by cnt, refill from the trace
+      int src = lane + cnt;
+      double a2 = __shfl_sync(FULLMASK, w_arr, src & 31);
+      int s2 = __shfl_sync(FULLMASK, w_s, src & 31);
+      int o2 = __shfl_sync(FULLMASK, w_o, src & 31);
+      if (src < 32) {
+        w_arr = a2;
+        w_s = s2;
+        w_o = o2;
+      } else {
+        load_rec(nxt + lane);
+      }
+      if (cnt < 32) break;
+    }
+  };
+
+  // ---- overloaded top-up until Def. 1 and the backlog hold (oracle.hpp:167-183)
+  auto topup = [&]() -> bool {
+    const long long freeslots = static_cast<long long>(G) * B - act;
+    while (!(n_wait >= min_pool && n_wait - maxcount >= freeslots)) {
+      long long idx = tail + lane;
+      bool valid = idx < N;
+      if (!__any_sync(FULLMASK, valid)) return false;
+      int s = 0, o = 0;
+      if (valid) {
+        int2 v = __ldg(reinterpret_cast<const int2*>(st) + idx);
+        s = v.x;
+        o = v.y;
+      }
+      unsigned peers = __match_any_sync(FULLMASK, valid ? s : -1 - lane);
+      long long base = valid ? static_cast<long long>(c_back[s] - c_front[s]) : 0;
+      unsigned le = lanemask_lt() | (1u << lane);
+      long long ncount = valid ? base + __popc(peers & le) : 0;
+      long long pm = ncount;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        long long v = __shfl_up_sync(FULLMASK, pm, off);
+        if (lane >= off && v > pm) pm = v;
+      }
+      long long mc = pm > maxcount ? pm : maxcount;
+      long long pool_j = n_wait + lane + 1;
+      bool cond = valid && pool_j >= min_pool && pool_j - mc >= freeslots;
+      unsigned cmask = __ballot_sync(FULLMASK, cond);
+      int take = cmask ? __ffs(cmask) : __popc(__ballot_sync(FULLMASK, valid));
+      unsigned tm = take >= 32 ? FULLMASK : ((1u << take) - 1u);
+      bool tk = lane < take;
+      int pos = 0, npeer = 0;
+      bool leader = false;
+      if (tk) {
+        unsigned p2 = peers & tm;
+        pos = c_back[s] + __popc(p2 & lanemask_lt());
+        npeer = __popc(p2);
+        leader = (__ffs(p2) - 1) == lane;
+      }
+      __syncwarp();
+      if (tk) {
+        if (GREEDY) deq[cbase[s] + pos] = make_int2(static_cast<int>(idx), o);
+        if (leader) c_back[s] = pos + npeer;
+        if (emit_reqs) {
+          P.reqs.arrival_step[ro + idx] = -1;
+          P.reqs.start_step[ro + idx] = -1;
+          P.reqs.worker[ro + idx] = -1;
+          P.reqs.admit_clock[ro + idx] = 0.0;
+          P.reqs.finish_clock[ro + idx] = 0.0;
+        }
+      }
+      if (GREEDY) wset.add_from_lanes(tk, tk ? s : 1);
+      maxcount = __shfl_sync(FULLMASK, mc, take - 1);
+      n_wait += take;
+      tail += take;
+      __syncwarp();
+    }
+    return true;
+  };
+
+  // Recompute the largest pool class after admissions (is_overloaded_at).
+  auto refresh_maxcount = [&]() {
+    long long m = 0;
+    for (int c = 1 + lane; c <= S; c += 32) {
+      long long v = c_back[c] - c_front[c];
+      m = v > m ? v : m;
+    }
+    maxcount = static_cast<long long>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(m)));
+  };
+
+  // place item (slot write + outputs); called by the item's lane
+  auto place = [&](int g, int rank, long long id, int s, int o) {
+    int slot = g * B + s_stk[g * B + s_capb[g] - 1 - rank];
+    s_f[slot] = static_cast<uint32_t>(k + o - 1);
+    s_a[slot] = static_cast<int32_t>(s - d * k);
+    s_x[slot] = static_cast<int32_t>(k);
+    s_id[slot] = static_cast<int32_t>(id);
+    if (emit_reqs) {
+      P.reqs.start_step[ro + id] = static_cast<int32_t>(k);
+      P.reqs.worker[ro + id] = g;
+      P.reqs.admit_clock[ro + id] = clock;
+    }
+  };
+
+  // ---- FCFS / JSQ: closed-form level filling (policies.hpp:100-138) ----
+  auto admit_fifo = [&](int U) {
+    int cap0[WPL];
+    int vext = JSQ ? INT_MAX : 0;
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+      int g = lane + 32 * j;
+      cap0[j] = g < G ? B - n[j] : 0;
+      if (g < G) s_capb[g] = cap0[j];
+      if (!JSQ) vext = cap0[j] > vext ? cap0[j] : vext;
+      else if (g < G && cap0[j] > 0 && n[j] < vext) vext = n[j];
+    }
+    int nl = 0, T = 0;
+    if (!JSQ) {
+      // Alg. 3: argmax cap, lowest index first. Level v (cap value, descending)
+      // serves every worker with cap0 >= v in index order.
+      int v = static_cast<int>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(vext)));
+      for (; v >= 1 && T < U; --v, ++nl) {
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          unsigned mk = __ballot_sync(FULLMASK, cap0[j] >= v);
+          cnt += __popc(mk);
+          if (lane == 0) lvM[nl * WPL + j] = mk;
+        }
+        int take = cnt < U - T ? cnt : U - T;
+        if (lane == 0) {
+          lvT[nl] = T;
+          lvV[nl] = v;
+          lvK[nl] = take;
+        }
+        T += take;
+      }
+    } else {
+      // JSQ: argmin active count over cap > 0, lowest index first. Level v
+      // (count value, ascending) serves every worker with count0 <= v < B.
+      int v = static_cast<int>(__reduce_min_sync(FULLMASK, static_cast<uint32_t>(vext)));
+      for (; v <= B - 1 && T < U; ++v, ++nl) {
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          int g = lane + 32 * j;
+          unsigned mk = __ballot_sync(FULLMASK, g < G && n[j] <= v);
+          cnt += __popc(mk);
+          if (lane == 0) lvM[nl * WPL + j] = mk;
+        }
+        int take = cnt < U - T ? cnt : U - T;
+        if (lane == 0) {
+          lvT[nl] = T;
+          lvV[nl] = v;
+          lvK[nl] = take;
+        }
+        T += take;
+      }
+    }
+    __syncwarp();
+    // item-parallel placement: admission t takes waiting request head + t
+    for (int t = lane; t < U; t += 32) {
+      int l = 0;
+      while (l + 1 < nl && lvT[l + 1] <= t) ++l;
+      int pos = t - lvT[l];
+      int g = 0;
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        uint32_t mk = lvM[l * WPL + j];
+        int c = __popc(mk);
+        if (pos >= 0 && pos < c) {
+          g = static_cast<int>(__fns(mk, 0, pos + 1)) + 32 * j;
+          pos = -1;
+        } else if (pos >= 0) {
+          pos -= c;
+        }
+      }
+      int rank = JSQ ? lvV[l] - (B - s_capb[g]) : s_capb[g] - lvV[l];
+      long long id = head + t;
+      int s, o;
+      if (OVL) {
+        int2 v = __ldg(reinterpret_cast<const int2*>(st) + id);
+        s = v.x;
+        o = v.y;
+        atomicAdd(&c_front[s], 1);  // leaves the pool (class count for Def. 1)
+      } else {
+        int4 v = __ldg(reinterpret_cast<const int4*>(tr) + id);
+        s = v.z;
+        o = v.w;
+      }
+      place(g, rank, id, s, o);
+      atomicAdd(&s_asum[g], static_cast<unsigned long long>(static_cast<long long>(s) - d * k));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+      int g = lane + 32 * j;
+      if (g >= G) continue;
+      int adm = 0;
+      for (int l = 0; l < nl; ++l) {
+        int before = 0;
+        bool mine = false;
+#pragma unroll
+        for (int j2 = 0; j2 < WPL; ++j2) {
+          uint32_t mk = lvM[l * WPL + j2];
+          if (j2 < j) before += __popc(mk);
+          if (j2 == j) {
+            mine = (mk >> lane) & 1u;
+            before += __popc(mk & lanemask_lt());
+          }
+        }
+        if (mine && before < lvK[l]) ++adm;
+      }
+      n[j] += adm;
+      A[j] += static_cast<long long>(s_asum[g]);
+      s_asum[g] = 0;
+    }
+    head += U;
+    __syncwarp();
+  };
+
+  // ---- bfio-greedy (policies.hpp:269-370) ----
+  auto admit_greedy = [&](int U, long long free_total) {
+    const bool phase1 = n_wait > free_total;
+    int cp[WPL];
+    long long F0[WPL];
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+      int g = lane + 32 * j;
+      cp[j] = g < G ? B - n[j] : 0;
+      F0[j] = g < G ? A[j] + d * k * n[j] : 0;
+      if (g < G) s_capb[g] = cp[j];
+    }
+    auto lane_key = [&](const long long* ld, const int* fr) -> uint64_t {
+      uint64_t best = ~0ull;
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        int g = lane + 32 * j;
+        if (g < G && fr[j] > 0) {
+          uint64_t kk = (static_cast<uint64_t>(ld[j]) << gbits) | static_cast<uint64_t>(g);
+          best = kk < best ? kk : best;
+        }
+      }
+      return best;
+    };
+    auto warp_argmin = [&](uint64_t key) -> uint64_t {
+      if (k32) {
+        uint32_t r = __reduce_min_sync(FULLMASK, key == ~0ull ? 0xFFFFFFFFu : static_cast<uint32_t>(key));
+        return r == 0xFFFFFFFFu ? ~0ull : static_cast<uint64_t>(r);
+      }
+      return wmin_u64(key);
+    };
+    __syncwarp();
+
+    if (phase1) {
+      // water filling (policies.hpp:274-323) restated over class deques (F4)
+      long long ld[WPL];
+      int fr[WPL];
+      long long tmax = 0;
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        ld[j] = F0[j];
+        fr[j] = cp[j];
+        tmax = ld[j] > tmax ? ld[j] : tmax;
+      }
+      long long target = static_cast<long long>(
+          __reduce_max_sync(FULLMASK, static_cast<uint32_t>(tmax)));
+      uint64_t lk = lane_key(ld, fr);
+      for (int q = 0; q < U; ++q) {
+        uint64_t km = warp_argmin(lk);
+        long long lmin = static_cast<long long>(km >> gbits);
+        int gs = static_cast<int>(km & gmask);
+        long long deficit = target - lmin;
+        int c = wset.highest_le(deficit);
+        bool back = c != 0;
+        if (!back) c = wset.lowest();
+        int fnt = c_front[c], bck = c_back[c];
+        int t = c_pc[c];
+        int idx;
+        if (back) {
+          --bck;
+          idx = bck;
+        } else {
+          idx = fnt;
+          ++fnt;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (back) c_back[c] = bck;
+          else c_front[c] = fnt;
+          c_pc[c] = t + 1;
+          p_idx[q] = cbase[c] + idx;
+          p_cl[q] = c;
+          p_t[q] = t;
+        }
+        if (fnt == bck) wset.clear(c);
+        if (t == 0) pset.add_uniform(c);
+#pragma unroll
+        for (int j = 0; j < WPL; ++j)
+          if (lane + 32 * j == gs) {
+            ld[j] += c;
+            fr[j] -= 1;
+          }
+        lk = lane_key(ld, fr);
+        long long nl = lmin + c;
+        target = nl > target ? nl : target;
+        __syncwarp();
+      }
+    }
+
+    int adm[WPL];
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) adm[j] = 0;
+    const long long ak = -d * k;  // a = s - d*x with x = k
+
+    if (H == 0) {
+      // placement (policies.hpp:339-367) at H = 0: argmin (load, index) over
+      // workers with a free slot (F3), items in w0-descending class order
+      uint64_t lk = lane_key(F0, cp);
+      int jpos = 0;
+      ClassSet<SMALLC>& set = phase1 ? pset : wset;
+      while (!set.empty()) {
+        int c = set.highest();
+        int nc, f0 = 0;
+        if (phase1) {
+          nc = c_pc[c];
+        } else {
+          f0 = c_front[c];
+          nc = c_back[c] - f0;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (phase1) {
+            c_cs[c] = jpos;
+            c_pc[c] = 0;
+          } else {
+            c_front[c] = c_back[c];
+          }
+        }
+        set.clear(c);
+        for (int t = 0; t < nc; ++t) {
+          uint64_t km = warp_argmin(lk);
+          int gs = static_cast<int>(km & gmask);
+#pragma unroll
+          for (int j = 0; j < WPL; ++j)
+            if (lane + 32 * j == gs) {
+              F0[j] += c;
+              cp[j] -= 1;
+              A[j] += c + ak;
+              s_res[jpos] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
+              adm[j] += 1;
+            }
+          if (!phase1 && lane == 0) {
+            p_idx[jpos] = cbase[c] + f0 + t;
+            p_cl[jpos] = c;
+          }
+          lk = lane_key(F0, cp);
+          ++jpos;
+        }
+      }
+      __syncwarp();
+      for (int q = lane; q < U; q += 32) {
+        int c = p_cl[q];
+        uint32_t r = s_res[phase1 ? c_cs[c] + p_t[q] : q];
+        int2 e = deq[p_idx[q]];
+        place(static_cast<int>(r & 0xFFFFu), static_cast<int>(r >> 16), e.x, c, e.y);
+      }
+    } else {
+      // general H: lookahead views F_h[g] from the finish window
+      const int H1 = H + 1;
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        int g = lane + 32 * j;
+        if (g >= G) continue;
+        long long PA = 0, PC = 0, Q = 0;
+        for (int h = 0; h <= H; ++h) {
+          if (h > 0) {
+            int r = static_cast<int>((k + h - 1) % Hm);
+            PA += s_Wa[r * G + g];
+            PC += s_Wc[r * G + g];
+            Q += PC;
+          }
+          long long kh = k + h;
+          long long F = trunc ? A[j] + d * kh * n[j] - d * Q
+                              : (A[j] + d * kh * n[j]) - (PA + d * kh * PC);
+          s_F[h * G + g] = F;
+        }
+      }
+      __syncwarp();
+      for (int h = lane; h <= H; h += 32) {
+        long long m = 0;
+        for (int g = 0; g < G; ++g) m = s_F[h * G + g] > m ? s_F[h * G + g] : m;
+        s_M[h] = m;
+      }
+      // ordered items: w0 descending, ties in pick order (phase 1) or waiting order
+      int jpos = 0;
+      ClassSet<SMALLC>& set = phase1 ? pset : wset;
+      while (!set.empty()) {
+        int c = set.highest();
+        int nc, f0 = 0;
+        if (phase1) {
+          nc = c_pc[c];
+        } else {
+          f0 = c_front[c];
+          nc = c_back[c] - f0;
+          for (int t = lane; t < nc; t += 32) {
+            int2 e = deq[cbase[c] + f0 + t];
+            o_c[jpos + t] = c;
+            o_o[jpos + t] = e.y;
+            o_id[jpos + t] = e.x;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (phase1) {
+            c_cs[c] = jpos;
+            c_pc[c] = 0;
+          } else {
+            c_front[c] = c_back[c];
+          }
+        }
+        set.clear(c);
+        jpos += nc;
+      }
+      __syncwarp();
+      if (phase1)
+        for (int q = lane; q < U; q += 32) {
+          int c = p_cl[q];
+          int jp = c_cs[c] + p_t[q];
+          int2 e = deq[p_idx[q]];
+          o_c[jp] = c;
+          o_o[jp] = e.y;
+          o_id[jp] = e.x;
+        }
+      __syncwarp();
+      for (int q = 0; q < U; ++q) {
+        const int c = o_c[q], o = o_o[q];
+        // lane-best (cost, F0, g) over owned workers with a free slot
+        uint64_t bc = ~0ull, bk = ~0ull;
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          int g = lane + 32 * j;
+          if (g >= G || cp[j] <= 0) continue;
+          long long cost = 0;
+          for (int h = 0; h <= H; ++h) {
+            long long w = h < o ? c + d * h : (trunc ? c + d * (o - 1) : 0);
+            long long v = s_F[h * G + g] + w;
+            long long m = s_M[h];
+            cost += v > m ? v : m;
+          }
+          uint64_t k2 = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
+          if (static_cast<uint64_t>(cost) < bc || (static_cast<uint64_t>(cost) == bc && k2 < bk)) {
+            bc = static_cast<uint64_t>(cost);
+            bk = k2;
+          }
+        }
+        uint64_t cmin = wmin_u64(bc);
+        uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
+        int gs = static_cast<int>(kmin & gmask);
+#pragma unroll
+        for (int j = 0; j < WPL; ++j)
+          if (lane + 32 * j == gs) {
+            for (int h = 0; h <= H; ++h) {
+              long long w = h < o ? c + d * h : (trunc ? c + d * (o - 1) : 0);
+              long long v = s_F[h * G + gs] + w;
+              s_F[h * G + gs] = v;
+              if (v > s_M[h]) s_M[h] = v;
+            }
+            cp[j] -= 1;
+            A[j] += c + ak;
+            s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
+            adm[j] += 1;
+            if (o <= H) {  // finishes inside the window [k, k+H-1]
+              int r = static_cast<int>((k + o - 1) % Hm);
+              s_Wc[r * G + gs] += 1;
+              s_Wa[r * G + gs] += c + ak;
+            }
+          }
+        __syncwarp();
+      }
+      for (int q = lane; q < U; q += 32) {
+        uint32_t r = s_res[q];
+        place(static_cast<int>(r & 0xFFFFu), static_cast<int>(r >> 16), o_id[q], o_c[q], o_o[q]);
+      }
+      (void)H1;
+    }
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) n[j] += adm[j];
+    __syncwarp();
+  };
+
+  // ---- retire requests finishing at step k (+ window entry at k + H) ----
+  auto retire = [&]() {
+    long long nd = 0;
+    double tp = 0.0;
+    const uint32_t kf = static_cast<uint32_t>(k);
+    const uint32_t kh = static_cast<uint32_t>(k + H);
+    const int rk = static_cast<int>(k % Hm);
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+      int g = lane + 32 * j;
+      if (g >= G) continue;
+      if (GREEDY && H > 0) {
+        s_Wc[rk * G + g] = 0;
+        s_Wa[rk * G + g] = 0;
+      }
+      if (n[j] == 0) continue;
+      const int base = g * B;
+      for (int i = 0; i < B; ++i) {
+        uint32_t f = s_f[base + i];
+        if (f == kf) {
+          int slot = base + i;
+          int x = s_x[slot];
+          A[j] -= s_a[slot];
+          int cap = B - n[j];
+          s_stk[base + cap] = static_cast<uint16_t>(i);
+          n[j] -= 1;
+          s_f[slot] = kEmpty;
+          // (finish - admit) / o per completed request (metrics.hpp:43-53)
+          double admit = ring[x & Rm];
+          tp = __dadd_rn(tp, __ddiv_rn(__dsub_rn(clock, admit), static_cast<double>(k - x + 1)));
+          ++nd;
+          if (emit_reqs) P.reqs.finish_clock[ro + s_id[slot]] = clock;
+        } else if (GREEDY && H > 0 && f == kh) {
+          s_Wc[rk * G + g] += 1;
+          s_Wa[rk * G + g] += s_a[base + i];
+        }
+      }
+    }
+    long long ndw = wsum_i64(nd);
+    done += ndw;
+    act -= ndw;
+    tpot_sum = __dadd_rn(tpot_sum, wsum_f64(tp));
+  };
+
+  // --- step loop -----------------------------------------------------------
+  for (;;) {
+    if (OVL) {
+      if (k >= total_steps) break;
+    } else {
+      if (done == N) break;  // all_done(), engine.hpp:171
+      if (k >= total_steps) {
+        status = BFSIM_PARTIAL;
+        break;
+      }
+    }
+    const double cs = clock;
+    if (OVL) {
+      if (!topup()) {
+        status = BFSIM_ESTREAM;
+        break;
+      }
+    } else {
+      reveal();
+    }
+    const long long free_total = static_cast<long long>(G) * B - act;
+    if (n_wait > 0 && free_total > 0) {
+      int U = static_cast<int>(n_wait < free_total ? n_wait : free_total);
+      if constexpr (GREEDY) admit_greedy(U, free_total);
+      else admit_fifo(U);
+      n_wait -= U;
+      act += U;
+      adm_total += U;
+      if (OVL) refresh_maxcount();
+    }
+    // loads, straggler max, dt, clock (engine.hpp:136-146)
+    uint32_t lmax = 0;
+    const int kr = static_cast<int>(k & 31);
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+      int g = lane + 32 * j;
+      if (g < G) {
+        uint32_t L = static_cast<uint32_t>(A[j] + d * k * n[j]);
+        r_l[kr * rstride + g] = L;
+        lmax = L > lmax ? L : lmax;
+      }
+    }
+    const uint32_t mx = __reduce_max_sync(FULLMASK, lmax);
+    const double dt = __dadd_rn(C0, __dmul_rn(TL, static_cast<double>(mx)));
+    clock = __dadd_rn(clock, dt);
+    if (lane == 0) {
+      r_dt[kr] = dt;
+      r_cs[kr] = cs;
+      r_mx[kr] = mx;
+      r_ac[kr] = static_cast<int32_t>(act);
+      ring[k & Rm] = cs;
+    }
+    __syncwarp();
+    if (kr == 31) flush(k - 31, 32);
+    if (act > 0 || (GREEDY && H > 0)) retire();
+    ++k;
+  }
+  if (k & 31) flush(k & ~31ll, static_cast<int>(k & 31));
+
+  // unrevealed requests (partial runs)
+  if (!OVL && emit_reqs)
+    for (long long id = nxt + lane; id < N; id += 32) {
+      P.reqs.arrival_step[ro + id] = -1;
+      P.reqs.start_step[ro + id] = -1;
+      P.reqs.worker[ro + id] = -1;
+      P.reqs.admit_clock[ro + id] = 0.0;
+      P.reqs.finish_clock[ro + id] = 0.0;
+    }
+
+  if (emit_steps && k > scap) flags |= BFSIM_FLAG_STEP_OVERFLOW;
+  if (lane == 0) {
+    bfsim_result_t r;
+    r.status = status;
+    r.flags = flags;
+    r.steps_run = k;
+    r.records = records;
+    r.completed = done;
+    r.admitted = adm_total;
+    r.consumed = OVL ? tail : nxt;
+    r.imb_total_i = imb;
+    r.total_workload_i = work;
+    r.tokens_i = tok;
+    r.clock = clock;
+    r.elapsed = elapsed;
+    r.tpot_sum = tpot_sum;
+    if (records == 0) {
+      r.flags |= BFSIM_FLAG_EMPTY;
+      r.avg_imbalance = r.throughput = r.tpot = r.energy = 0.0;
+      r.imb_total = r.total_workload = r.eta_sum = 0.0;
+    } else {
+      // compute_metrics, metrics.hpp:106-122
+      r.avg_imbalance = static_cast<double>(imb) / static_cast<double>(records);
+      r.throughput = static_cast<double>(tok) / elapsed;
+      r.tpot = done > 0 ? tpot_sum / static_cast<double>(done) : 0.0;
+      r.energy = energy;
+      r.imb_total = static_cast<double>(imb);
+      r.total_workload = static_cast<double>(work);
+      r.eta_sum = work > 0 ? static_cast<double>(imb) / static_cast<double>(work) : 0.0;
+    }
+    P.results[si] = r;
+  }
+  __syncwarp();
+}
+
+template <int MODE, int POL, int WPL, bool SMALLC>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    step_kernel(KParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int wpc = blockDim.x >> 5;
+  unsigned char* sm = smem + static_cast<size_t>(warp) * P.plan.smem_per_warp;
+  unsigned char* ws =
+      P.ws + static_cast<size_t>(blockIdx.x * wpc + warp) * P.plan.ws_stride;
+  for (;;) {
+    int qi = 0;
+    if (lane == 0) qi = atomicAdd(P.queue, 1);
+    qi = __shfl_sync(FULLMASK, qi, 0);
+    if (qi >= P.n) break;
+    run_traj<MODE, POL, WPL, SMALLC>(P, P.order[qi], sm, ws);
+  }
+}
+
+template <int MODE, int POL, int WPL, bool SMALLC>
+int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
+  auto fn = step_kernel<MODE, POL, WPL, SMALLC>;
+  size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * wpc;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  if (occ) {  // occupancy query only
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, wpc * 32, smem);
+    return static_cast<int>(e);
+  }
+  fn<<<grid, wpc * 32, smem, s>>>(kp);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Only bfio-greedy uses the class bitmaps, so the FIFO families ignore `small`.
+template <int MODE, int POL>
+int launch_family(int wpl, int small, const KParams& kp, int grid, int wpc, cudaStream_t s,
+                  int* occ) {
+  constexpr bool kClasses = POL == BFSIM_POLICY_BFIO_GREEDY;
+  if (kClasses && !small) {
+    switch (wpl) {
+      case 1: return launch_t<MODE, POL, 1, false>(kp, grid, wpc, s, occ);
+      case 2: return launch_t<MODE, POL, 2, false>(kp, grid, wpc, s, occ);
+      case 4: return launch_t<MODE, POL, 4, false>(kp, grid, wpc, s, occ);
+      case 8: return launch_t<MODE, POL, 8, false>(kp, grid, wpc, s, occ);
+    }
+    return static_cast<int>(cudaErrorInvalidValue);
+  }
+  switch (wpl) {
+    case 1: return launch_t<MODE, POL, 1, true>(kp, grid, wpc, s, occ);
+    case 2: return launch_t<MODE, POL, 2, true>(kp, grid, wpc, s, occ);
+    case 4: return launch_t<MODE, POL, 4, true>(kp, grid, wpc, s, occ);
+    case 8: return launch_t<MODE, POL, 8, true>(kp, grid, wpc, s, occ);
+  }
+  return static_cast<int>(cudaErrorInvalidValue);
+}
+
+}  // namespace detail
+
+#define BFSIM_DECLARE_FAMILY(M, P)                                                            \
+  int launch_family_##M##_##P(int wpl, int small, const KParams& kp, int grid, int wpc,       \
+                              cudaStream_t s, int* occ);
+BFSIM_DECLARE_FAMILY(0, 0)
+BFSIM_DECLARE_FAMILY(0, 1)
+BFSIM_DECLARE_FAMILY(0, 3)
+BFSIM_DECLARE_FAMILY(1, 0)
+BFSIM_DECLARE_FAMILY(1, 1)
+BFSIM_DECLARE_FAMILY(1, 3)
+
+}  // namespace bfsim
