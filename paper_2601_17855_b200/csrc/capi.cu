@@ -186,15 +186,17 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   std::vector<Item> items = {
       {&p.o_rl, 32LL * rstride * 4}, {&p.o_rdt, 32 * 8}, {&p.o_rcs, 32 * 8}, {&p.o_rmx, 32 * 4},
       {&p.o_rac, 32 * 4},            {&p.o_capb, G * 4LL}, {&p.o_asum, G * 8LL},
+      {&p.o_cap, G * 4LL},           {&p.o_rn, G * 4LL},  {&p.o_rlist, GB * 2},
       {&p.o_lvT, lvl * 4},           {&p.o_lvV, lvl * 4}, {&p.o_lvK, lvl * 4},
-      {&p.o_lvM, lvl * wpl * 4},     {&p.o_f, GB * 4},    {&p.o_stk, GB * 2},
+      {&p.o_lvM, lvl * wpl * 4},     {&p.o_f, ((GB + 3) & ~3LL) * 4},    {&p.o_stk, GB * 2},
       {&p.o_a, GB * 4},              {&p.o_x, GB * 4},    {&p.o_id, GB * 4},
   };
   if (greedy || ovl) {
-    items.push_back({&p.o_cls, 4LL * (S + 2) * 4});
+    items.push_back({&p.o_cls, 5LL * (S + 2) * 4});  // int4 records + int32 starts
     items.push_back({&p.o_bm, bm_words * 8});
     items.push_back({&p.o_pbm, bm_words * 8});
   }
+  items.push_back({&p.o_stage, GB * 8});
   if (greedy && H > 0) {
     items.push_back({&p.o_M, (H + 1) * 8LL});
     items.push_back({&p.o_F, (H + 1) * 8LL * G});
@@ -203,7 +205,6 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   }
   if (greedy) {
     items.push_back({&p.o_res, GB * 4});
-    items.push_back({&p.o_pidx, GB * 4});
     items.push_back({&p.o_pcl, GB * 4});
     items.push_back({&p.o_pt, GB * 4});
     if (H > 0) {
@@ -214,16 +215,19 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   }
   items.push_back({&p.o_ring, R * 8LL});
   int64_t sm_off = 0, ws_off = 0;
+  int spilled = 0;
   for (auto& it : items) {
     int64_t b = (it.bytes + 15) & ~15LL;
-    if (sm_off + b <= smem_budget) {
+    if (!spilled && sm_off + b <= smem_budget) {
       *it.code = sm_off;
       sm_off += b;
     } else {
       *it.code = -(ws_off + 1);
       ws_off += b;
+      spilled = 1;
     }
   }
+  p.all_smem = spilled ? 0 : 1;
   if (greedy) {  // per-class waiting deques: counting-sort layout over the input
     int64_t b = ((max_len * 8) + 15) & ~15LL;
     p.o_deq = -(ws_off + 1);
@@ -357,9 +361,17 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
              est_work(scen_host[b], inputs_host[scen_host[b].input_id]);
     });
     // shared memory: up to 4 warps per CTA within the opt-in limit
-    int budget = std::min(ctx->smem_optin / 4 - 64, 200 * 1024);
+    // shared-memory budget per trajectory: enough trajectories resident per SM
+    // to hold the whole group at once (latency-bound warps), the rest spills
+    // to the per-warp global workspace
+    int64_t per_sm = (static_cast<int64_t>(g.idx.size()) + ctx->sm_count - 1) / ctx->sm_count;
+    per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, 16));
+    int budget = static_cast<int>(std::min<int64_t>(ctx->smem_optin - 1024,
+                                                    (228 * 1024) / per_sm - 2048));
+    budget = std::max(budget, 8 * 1024);
     make_plan(g, scen_host, inputs_host, budget);
-    g.wpc = std::max(1, std::min(4, ctx->smem_optin / std::max(1, g.plan.smem_per_warp)));
+    // one warp (trajectory) per CTA: latency-bound warps spread over every SM
+    g.wpc = 1;
     KParams probe{};
     probe.plan = g.plan;
     int occ = 0;

@@ -19,18 +19,19 @@ struct Plan {
   int R;           // clock ring entries (power of two > max decode)
   int umax;        // max admissions in one step (G*B)
   int smem_per_warp;
-  int reserved;
+  int all_smem;  // every array placed in shared memory (32-bit addressing variant)
   int64_t ws_stride;
   // slots
-  int64_t o_f, o_a, o_x, o_id, o_stk, o_capb, o_asum;
+  int64_t o_f, o_a, o_x, o_id, o_stk, o_capb, o_asum, o_cap, o_rn, o_rlist;
   // per-step accounting ring (32 steps) and clock ring
   int64_t o_rl, o_rdt, o_rcs, o_rmx, o_rac, o_ring;
   // FCFS/JSQ level tables
   int64_t o_lvT, o_lvV, o_lvK, o_lvM;
-  // class structures: 4 int32 arrays of S+2 (front, back, picks, start) + 2 bitmaps
+  // class structures: int4 records {front, back, picks, base} + int32 chain start, S+2 each; 2 bitmaps;
+  // o_deq (per-class waiting deques) is always in the global workspace
   int64_t o_cls, o_bm, o_pbm, o_deq;
-  // picks / chain results
-  int64_t o_pidx, o_pcl, o_pt, o_res;
+  // picks / chain results / prefetch stage (int2 per admission)
+  int64_t o_stage, o_pcl, o_pt, o_res;
   // lookahead window (H > 0)
   int64_t o_F, o_M, o_Wc, o_Wa, o_oc, o_oo, o_oid;
 };

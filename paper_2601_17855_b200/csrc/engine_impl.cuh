@@ -1,13 +1,15 @@
 #pragma once
 // B200 (sm_100a) batched step engine for the BF-IO hot path.
 //
-// One warp simulates one trajectory (scenario) end to end; persistent warps
-// pull scenarios from an atomic queue. Worker g is owned by lane g % 32 (slot
-// j = g / 32 of WPL register-resident workers per lane), so per-worker state
-// (active count, load aggregate) lives in registers and every per-worker
-// update is lane-local. Per-slot, per-class and lookahead-window state lives in
-// the warp's shared-memory arena; the per-prefill-class waiting deques live in
-// a per-warp global workspace (L2-resident).
+// One warp simulates one trajectory (scenario) end to end; persistent CTAs of
+// one warp pull scenarios from an atomic queue. Worker g is owned by lane
+// g % 32 (slot j = g / 32 of WPL register-resident workers per lane), so
+// per-worker state (active count, load aggregate) lives in registers and every
+// per-worker update is lane-local. Per-slot, per-class and lookahead-window
+// state lives in the warp's shared-memory arena (SM = true: 32-bit LDS/STS);
+// the per-prefill-class waiting deques live in a per-warp global workspace
+// (L2-resident) and the records an admission needs are prefetched into shared
+// memory with cp.async while the sequential placement chain runs.
 //
 // Reference semantics (paths under /root/reference/proj/include/bfsim/):
 //   step order            engine.hpp:112-160 (Poisson), oracle.hpp:163-242 (overloaded)
@@ -22,6 +24,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "engine.cuh"
 
@@ -46,6 +49,16 @@ __device__ __forceinline__ uint64_t wmin_u64(uint64_t v) {
   return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
+// warp argmin of packed (value << gbits | g) keys; K32: every key fits 31 bits
+template <bool K32>
+__device__ __forceinline__ uint64_t argmin_key(uint64_t key) {
+  if constexpr (K32) {
+    return static_cast<uint64_t>(__reduce_min_sync(FULLMASK, static_cast<uint32_t>(key)));
+  } else {
+    return wmin_u64(key);
+  }
+}
+
 __device__ __forceinline__ long long wsum_i64(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
@@ -58,22 +71,36 @@ __device__ __forceinline__ double wsum_f64(double v) {
   return v;
 }
 
-// Array placement code from the planner: >= 0 is a byte offset into the warp's
-// shared-memory arena, < 0 encodes (-code - 1) bytes into its global workspace.
-template <class T>
-__device__ __forceinline__ T* at(unsigned char* sm, unsigned char* ws, int64_t code) {
-  return code >= 0 ? reinterpret_cast<T*>(sm + code) : reinterpret_cast<T*>(ws + (-code - 1));
-}
-
 __device__ __forceinline__ int bits_for(long long x) {  // bits to hold values 0..x
   return x <= 0 ? 0 : 64 - __clzll(static_cast<unsigned long long>(x));
 }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// Array placement from the planner. SM: every code is a shared-memory offset,
+// so the compiler emits 32-bit shared loads/stores. Otherwise a code < 0 is
+// byte (-code - 1) of the warp's global workspace.
+template <bool SM, class T>
+__device__ __forceinline__ T* at(unsigned char* sm, unsigned char* ws, int64_t code) {
+  if constexpr (SM) {
+    return reinterpret_cast<T*>(sm + code);
+  } else {
+    return code >= 0 ? reinterpret_cast<T*>(sm + code) : reinterpret_cast<T*>(ws + (-code - 1));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Set of non-empty prefill classes c = 1..S (bit c-1). SMALL: S <= 64 in one
-// register word. Otherwise a 3-level 64-ary bitmap (top word in a register,
-// mid/leaf words in shared or global memory). All lanes execute every
-// operation uniformly; lane 0 performs the stores.
+// uniform register word. Otherwise a 3-level 64-ary bitmap (top word in a
+// register, mid/leaf words in memory). Every operation is executed uniformly
+// by all lanes; stores write the same value from every lane, so a lane's later
+// load sees its own store without a warp barrier.
 template <bool SMALL>
 struct ClassSet;
 
@@ -85,12 +112,10 @@ struct ClassSet<true> {
   __device__ int highest() const { return bits ? 64 - __clzll(bits) : 0; }
   __device__ int lowest() const { return bits ? __ffsll(static_cast<long long>(bits)) : 0; }
   __device__ int highest_le(long long d) const {
-    if (d < 1) return 0;
-    uint64_t m = d >= 64 ? bits : (bits & ((1ull << d) - 1ull));
+    uint64_t m = d >= 64 ? bits : (d < 1 ? 0ull : (bits & ((1ull << d) - 1ull)));
     return m ? 64 - __clzll(m) : 0;
   }
   __device__ void clear(int c) { bits &= ~(1ull << (c - 1)); }
-  // lanes with `has` contribute class c; result is uniform
   __device__ void add_from_lanes(bool has, int c) {
     uint64_t m = has ? (1ull << (c - 1)) : 0ull;
     uint32_t lo = __reduce_or_sync(FULLMASK, static_cast<uint32_t>(m));
@@ -156,20 +181,18 @@ struct ClassSet<false> {
     return tm ? from_top(tm) : 0;
   }
   __device__ void clear(int c) {
-    const int lane = threadIdx.x & 31;
     int b = c - 1, w = b >> 6;
     uint64_t lw = leaf[w] & ~(1ull << (b & 63));
-    uint64_t m2 = mid[w >> 6] & ~(1ull << (w & 63));
-    __syncwarp();
-    if (lane == 0) leaf[w] = lw;
+    leaf[w] = lw;
     if (lw == 0) {
-      if (lane == 0) mid[w >> 6] = m2;
+      uint64_t m2 = mid[w >> 6] & ~(1ull << (w & 63));
+      mid[w >> 6] = m2;
       if (m2 == 0) top &= ~(1ull << (w >> 6));
     }
-    __syncwarp();
   }
   __device__ void add_from_lanes(bool has, int c) {
     uint64_t tb = 0;
+    __syncwarp();
     if (has) {
       int b = c - 1, w = b >> 6;
       atomicOr(reinterpret_cast<unsigned long long*>(&leaf[w]), 1ull << (b & 63));
@@ -182,21 +205,16 @@ struct ClassSet<false> {
     __syncwarp();
   }
   __device__ void add_uniform(int c) {
-    const int lane = threadIdx.x & 31;
     int b = c - 1, w = b >> 6;
-    __syncwarp();
-    if (lane == 0) {
-      leaf[w] |= 1ull << (b & 63);
-      mid[w >> 6] |= 1ull << (w & 63);
-    }
+    leaf[w] |= 1ull << (b & 63);
+    mid[w >> 6] |= 1ull << (w & 63);
     top |= 1ull << (w >> 6);
-    __syncwarp();
   }
 };
 
 // ---------------------------------------------------------------------------
 
-template <int MODE, int POL, int WPL, bool SMALLC>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM>
 __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned char* ws) {
   constexpr bool OVL = MODE == BFSIM_MODE_OVERLOADED;
   constexpr bool GREEDY = POL == BFSIM_POLICY_BFIO_GREEDY;
@@ -214,7 +232,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   const long long N = in.length;
   const bfsim_request_t* tr = P.traces ? P.traces + in.offset : nullptr;
   const bfsim_sample_t* st = P.streams ? P.streams + in.offset : nullptr;
-  const int32_t* cbase = P.class_base + in.class_base_offset;
+  const int32_t* cbase_g = P.class_base + in.class_base_offset;
   const double C0 = sc.overhead, TL = sc.per_token;
   const double p_idle = sc.p_idle, p_diff = sc.p_max - sc.p_idle, gam = sc.gamma;
   const long long warmup = OVL ? sc.warmup : 0;
@@ -225,65 +243,69 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   const long long so = sc.step_offset, scap = sc.step_capacity, lo = sc.load_offset;
   const long long ro = sc.req_offset;
   const int rstride = (G & 1) ? G : G + 1;  // padded accounting-ring row (bank conflicts)
+  const int umax = pl.umax;
+  const float invB = 1.0f / static_cast<float>(B);
 
-  // --- arenas (shared memory, or the warp's global workspace when too big) --
-  uint32_t* s_f = at<uint32_t>(sm, ws, pl.o_f);
-  int32_t* s_a = at<int32_t>(sm, ws, pl.o_a);
-  int32_t* s_x = at<int32_t>(sm, ws, pl.o_x);
-  int32_t* s_id = at<int32_t>(sm, ws, pl.o_id);
-  uint16_t* s_stk = at<uint16_t>(sm, ws, pl.o_stk);
-  int32_t* s_capb = at<int32_t>(sm, ws, pl.o_capb);
-  unsigned long long* s_asum = at<unsigned long long>(sm, ws, pl.o_asum);
-  uint32_t* r_l = at<uint32_t>(sm, ws, pl.o_rl);
-  double* r_dt = at<double>(sm, ws, pl.o_rdt);
-  double* r_cs = at<double>(sm, ws, pl.o_rcs);
-  uint32_t* r_mx = at<uint32_t>(sm, ws, pl.o_rmx);
-  int32_t* r_ac = at<int32_t>(sm, ws, pl.o_rac);
-  double* ring = at<double>(sm, ws, pl.o_ring);
+  // --- arenas --------------------------------------------------------------
+  uint32_t* s_f = at<SM, uint32_t>(sm, ws, pl.o_f);
+  int32_t* s_a = at<SM, int32_t>(sm, ws, pl.o_a);
+  int32_t* s_x = at<SM, int32_t>(sm, ws, pl.o_x);
+  int32_t* s_id = at<SM, int32_t>(sm, ws, pl.o_id);
+  uint16_t* s_stk = at<SM, uint16_t>(sm, ws, pl.o_stk);
+  int32_t* s_capb = at<SM, int32_t>(sm, ws, pl.o_capb);
+  unsigned long long* s_asum = at<SM, unsigned long long>(sm, ws, pl.o_asum);
+  int32_t* s_cap = at<SM, int32_t>(sm, ws, pl.o_cap);
+  int32_t* s_rn = at<SM, int32_t>(sm, ws, pl.o_rn);
+  uint32_t* r_l = at<SM, uint32_t>(sm, ws, pl.o_rl);
+  double* r_dt = at<SM, double>(sm, ws, pl.o_rdt);
+  double* r_cs = at<SM, double>(sm, ws, pl.o_rcs);
+  uint32_t* r_mx = at<SM, uint32_t>(sm, ws, pl.o_rmx);
+  int32_t* r_ac = at<SM, int32_t>(sm, ws, pl.o_rac);
+  double* ring = at<SM, double>(sm, ws, pl.o_ring);
   const int Rm = pl.R - 1;
-  int32_t* c_front = at<int32_t>(sm, ws, pl.o_cls);
-  int32_t* c_back = c_front + (pl.S + 2);
-  int32_t* c_pc = c_back + (pl.S + 2);
-  int32_t* c_cs = c_pc + (pl.S + 2);
-  int2* deq = at<int2>(sm, ws, pl.o_deq);
-  int32_t* p_idx = at<int32_t>(sm, ws, pl.o_pidx);
-  int32_t* p_cl = at<int32_t>(sm, ws, pl.o_pcl);
-  int32_t* p_t = at<int32_t>(sm, ws, pl.o_pt);
-  uint32_t* s_res = at<uint32_t>(sm, ws, pl.o_res);
-  int32_t* lvT = at<int32_t>(sm, ws, pl.o_lvT);
-  int32_t* lvV = at<int32_t>(sm, ws, pl.o_lvV);
-  int32_t* lvK = at<int32_t>(sm, ws, pl.o_lvK);
-  uint32_t* lvM = at<uint32_t>(sm, ws, pl.o_lvM);
-  long long* s_F = at<long long>(sm, ws, pl.o_F);
-  long long* s_M = at<long long>(sm, ws, pl.o_M);
-  int32_t* s_Wc = at<int32_t>(sm, ws, pl.o_Wc);
-  long long* s_Wa = at<long long>(sm, ws, pl.o_Wa);
-  int32_t* o_c = at<int32_t>(sm, ws, pl.o_oc);
-  int32_t* o_o = at<int32_t>(sm, ws, pl.o_oo);
-  int32_t* o_id = at<int32_t>(sm, ws, pl.o_oid);
+  // per-class record {front, back, picks this step, deque base} + chain start
+  int4* c_rec = at<SM, int4>(sm, ws, pl.o_cls);
+  int32_t* c_cs = reinterpret_cast<int32_t*>(c_rec + (pl.S + 2));
+  uint16_t* s_rlist = at<SM, uint16_t>(sm, ws, pl.o_rlist);
+  int2* deq = reinterpret_cast<int2*>(ws + (-pl.o_deq - 1));
+  int2* stage = at<SM, int2>(sm, ws, pl.o_stage);  // prefetched (id|s, o) records
+  int32_t* p_cl = at<SM, int32_t>(sm, ws, pl.o_pcl);
+  int32_t* p_t = at<SM, int32_t>(sm, ws, pl.o_pt);
+  uint32_t* s_res = at<SM, uint32_t>(sm, ws, pl.o_res);
+  int32_t* lvT = at<SM, int32_t>(sm, ws, pl.o_lvT);
+  int32_t* lvV = at<SM, int32_t>(sm, ws, pl.o_lvV);
+  int32_t* lvK = at<SM, int32_t>(sm, ws, pl.o_lvK);
+  uint32_t* lvM = at<SM, uint32_t>(sm, ws, pl.o_lvM);
+  long long* s_F = at<SM, long long>(sm, ws, pl.o_F);
+  long long* s_M = at<SM, long long>(sm, ws, pl.o_M);
+  int32_t* s_Wc = at<SM, int32_t>(sm, ws, pl.o_Wc);
+  long long* s_Wa = at<SM, long long>(sm, ws, pl.o_Wa);
+  int32_t* o_c = at<SM, int32_t>(sm, ws, pl.o_oc);
+  int32_t* o_o = at<SM, int32_t>(sm, ws, pl.o_oo);
+  int32_t* o_id = at<SM, int32_t>(sm, ws, pl.o_oid);
 
   // --- init ----------------------------------------------------------------
-  for (int i = lane; i < G * B; i += 32) {
+  for (int i = lane; i < ((G * B + 3) & ~3); i += 32) {
     s_f[i] = kEmpty;
-    s_stk[i] = static_cast<uint16_t>(i % B);
+    if (i < G * B) s_stk[i] = static_cast<uint16_t>(i % B);
   }
-  const bool use_classes = GREEDY || OVL;
-  if (use_classes)
-    for (int c = lane; c <= S + 1; c += 32) {
-      c_front[c] = 0;
-      c_back[c] = 0;
-      c_pc[c] = 0;
-    }
+  for (int i = lane; i < G; i += 32) {
+    s_cap[i] = B;
+    s_rn[i] = 0;
+    s_asum[i] = 0;
+  }
+  constexpr bool kClasses = GREEDY || OVL;
+  if (kClasses)
+    for (int c = lane; c <= S + 1; c += 32) c_rec[c] = make_int4(0, 0, 0, GREEDY ? cbase_g[c] : 0);
   if (GREEDY && H > 0)
     for (int i = lane; i < H * G; i += 32) {
       s_Wc[i] = 0;
       s_Wa[i] = 0;
     }
-  for (int i = lane; i < G; i += 32) s_asum[i] = 0;
   ClassSet<SMALLC> wset, pset;  // waiting classes; classes picked in phase 1
   {
-    uint64_t* bm = at<uint64_t>(sm, ws, pl.o_bm);
-    uint64_t* pbm = at<uint64_t>(sm, ws, pl.o_pbm);
+    uint64_t* bm = at<SM, uint64_t>(sm, ws, pl.o_bm);
+    uint64_t* pbm = at<SM, uint64_t>(sm, ws, pl.o_pbm);
     wset.init(bm, bm + 64, S);
     pset.init(pbm, pbm + 64, S);
   }
@@ -314,18 +336,21 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int status = BFSIM_OK;
   uint32_t flags = 0;
 
-  // reveal window: lane j holds trace record nxt + j
-  double w_arr = 0.0;
-  int w_s = 0, w_o = 0;
-  auto load_rec = [&](long long idx) {
-    if (idx < N) {
-      int4 v = __ldg(reinterpret_cast<const int4*>(tr) + idx);
-      w_arr = __hiloint2double(v.y, v.x);
-      w_s = v.z;
-      w_o = v.w;
-    }
+  // Reveal windows: lane j holds trace records nxt + j (A, unpacked) and
+  // nxt + 32 + j (B, raw 16-byte record still in flight from the trace).
+  double a_arr = 0.0;
+  int a_s = 0, a_o = 0;
+  int4 b4 = make_int4(0, 0, 0, 0);
+  auto load_raw = [&](long long idx) -> int4 {
+    return idx < N ? __ldg(reinterpret_cast<const int4*>(tr) + idx) : make_int4(0, 0, 0, 0);
   };
-  if (!OVL) load_rec(lane);
+  if (!OVL) {
+    const int4 v = load_raw(lane);
+    a_arr = __hiloint2double(v.y, v.x);
+    a_s = v.z;
+    a_o = v.w;
+    b4 = load_raw(32 + lane);
+  }
 
   // ---- per-step accounting flush: steps k0 .. k0+cnt-1 in ring rows 0..cnt-1
   auto flush = [&](long long k0, int cnt) {
@@ -388,7 +413,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   // ---- Poisson reveal (engine.hpp:123-128) ----
   auto reveal = [&]() {
     for (;;) {
-      bool ok = (nxt + lane < N) && (w_arr <= clock);
+      bool ok = (nxt + lane < N) && (a_arr <= clock);
       unsigned m = __ballot_sync(FULLMASK, ok);
       int cnt = __popc(m);  // arrivals sorted: m is a prefix of the lanes
       if (cnt == 0) break;
@@ -404,33 +429,49 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         // push to the back of the per-class deque, arrival order within class
         int pos = 0, npeer = 0;
         bool leader = false;
+        int cbase = 0;
         if (ok) {
-          unsigned peers = __match_any_sync(m, w_s);
-          pos = c_back[w_s] + __popc(peers & lanemask_lt());
+          unsigned peers = __match_any_sync(m, a_s);
+          const int4 cr = c_rec[a_s];
+          pos = cr.y + __popc(peers & lanemask_lt());
+          cbase = cr.w;
           npeer = __popc(peers);
           leader = (__ffs(peers) - 1) == lane;
         }
         __syncwarp();
         if (ok) {
-          deq[cbase[w_s] + pos] = make_int2(static_cast<int>(id), w_o);
-          if (leader) c_back[w_s] = pos + npeer;
+          deq[cbase + pos] = make_int2(static_cast<int>(id), a_o);
+          if (leader) c_rec[a_s].y = pos + npeer;
         }
-        wset.add_from_lanes(ok, ok ? w_s : 1);
+        wset.add_from_lanes(ok, ok ? a_s : 1);
         __syncwarp();
+      } else {
+        // stash (s, o) for the FIFO admission: slot = position in the queue
+        long long t = id - head;
+        if (ok && t < umax) stage[t] = make_int2(a_s, a_o);
       }
       n_wait += cnt;
       nxt += cnt;
-      // shift the window by cnt, refill from the trace
-      int src = lane + cnt;
-      double a2 = __shfl_sync(FULLMASK, w_arr, src & 31);
-      int s2 = __shfl_sync(FULLMASK, w_s, src & 31);
-      int o2 = __shfl_sync(FULLMASK, w_o, src & 31);
-      if (src < 32) {
-        w_arr = a2;
-        w_s = s2;
-        w_o = o2;
+      // shift both windows by cnt; refill the tail of B from the trace
+      const int src = (lane + cnt) & 31;
+      const bool fromA = lane + cnt < 32;
+      const double xa = __shfl_sync(FULLMASK, a_arr, src);
+      const int sa = __shfl_sync(FULLMASK, a_s, src), oa = __shfl_sync(FULLMASK, a_o, src);
+      int4 vb;
+      vb.x = __shfl_sync(FULLMASK, b4.x, src);
+      vb.y = __shfl_sync(FULLMASK, b4.y, src);
+      vb.z = __shfl_sync(FULLMASK, b4.z, src);
+      vb.w = __shfl_sync(FULLMASK, b4.w, src);
+      if (fromA) {
+        a_arr = xa;
+        a_s = sa;
+        a_o = oa;
+        b4 = vb;
       } else {
-        load_rec(nxt + lane);
+        a_arr = __hiloint2double(vb.y, vb.x);
+        a_s = vb.z;
+        a_o = vb.w;
+        b4 = load_raw(nxt + 32 + lane);
       }
       if (cnt < 32) break;
     }
@@ -450,7 +491,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         o = v.y;
       }
       unsigned peers = __match_any_sync(FULLMASK, valid ? s : -1 - lane);
-      long long base = valid ? static_cast<long long>(c_back[s] - c_front[s]) : 0;
+      int4 cr = valid ? c_rec[s] : make_int4(0, 0, 0, 0);
+      long long base = static_cast<long long>(cr.y - cr.x);
       unsigned le = lanemask_lt() | (1u << lane);
       long long ncount = valid ? base + __popc(peers & le) : 0;
       long long pm = ncount;
@@ -470,14 +512,19 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       bool leader = false;
       if (tk) {
         unsigned p2 = peers & tm;
-        pos = c_back[s] + __popc(p2 & lanemask_lt());
+        pos = cr.y + __popc(p2 & lanemask_lt());
         npeer = __popc(p2);
         leader = (__ffs(p2) - 1) == lane;
       }
       __syncwarp();
       if (tk) {
-        if (GREEDY) deq[cbase[s] + pos] = make_int2(static_cast<int>(idx), o);
-        if (leader) c_back[s] = pos + npeer;
+        if (GREEDY) {
+          deq[cr.w + pos] = make_int2(static_cast<int>(idx), o);
+        } else {
+          long long t = idx - head;
+          if (t < umax) stage[t] = make_int2(s, o);
+        }
+        if (leader) c_rec[s].y = pos + npeer;
         if (emit_reqs) {
           P.reqs.arrival_step[ro + idx] = -1;
           P.reqs.start_step[ro + idx] = -1;
@@ -499,7 +546,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   auto refresh_maxcount = [&]() {
     long long m = 0;
     for (int c = 1 + lane; c <= S; c += 32) {
-      long long v = c_back[c] - c_front[c];
+      const int4 cr = c_rec[c];
+      long long v = cr.y - cr.x;
       m = v > m ? v : m;
     }
     maxcount = static_cast<long long>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(m)));
@@ -516,6 +564,21 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       P.reqs.start_step[ro + id] = static_cast<int32_t>(k);
       P.reqs.worker[ro + id] = g;
       P.reqs.admit_clock[ro + id] = clock;
+    }
+  };
+
+  // FIFO policies: prefetch the (s, o) of the next step's oldest waiting
+  // requests (already revealed) into the stage while the tail of this step runs.
+  auto prefetch_fifo = [&]() {
+    if constexpr (!GREEDY && SM) {
+      long long freeslots = static_cast<long long>(G) * B - act;
+      long long np = n_wait < freeslots ? n_wait : freeslots;
+      np = np < umax ? np : umax;
+      for (long long t = lane; t < np; t += 32) {
+        const void* src = OVL ? static_cast<const void*>(st + head + t)
+                              : static_cast<const void*>(&tr[head + t].prefill);
+        cp_async8(&stage[t], src);
+      }
     }
   };
 
@@ -574,6 +637,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         T += take;
       }
     }
+    if (SM) cp_async_wait_all();
     __syncwarp();
     // item-parallel placement: admission t takes waiting request head + t
     for (int t = lane; t < U; t += 32) {
@@ -595,16 +659,20 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       int rank = JSQ ? lvV[l] - (B - s_capb[g]) : s_capb[g] - lvV[l];
       long long id = head + t;
       int s, o;
-      if (OVL) {
+      if (SM && t < umax) {
+        int2 v = stage[t];
+        s = v.x;
+        o = v.y;
+      } else if (OVL) {
         int2 v = __ldg(reinterpret_cast<const int2*>(st) + id);
         s = v.x;
         o = v.y;
-        atomicAdd(&c_front[s], 1);  // leaves the pool (class count for Def. 1)
       } else {
         int4 v = __ldg(reinterpret_cast<const int4*>(tr) + id);
         s = v.z;
         o = v.w;
       }
+      if (OVL) atomicAdd(&c_rec[s].x, 1);  // leaves the pool (class count for Def. 1)
       place(g, rank, id, s, o);
       atomicAdd(&s_asum[g], static_cast<unsigned long long>(static_cast<long long>(s) - d * k));
     }
@@ -637,7 +705,11 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   };
 
   // ---- bfio-greedy (policies.hpp:269-370) ----
-  auto admit_greedy = [&](int U, long long free_total) {
+  // Keys are (load << gbits | g), 32-bit when every load fits (K32).
+  auto admit_greedy = [&](int U, long long free_total, auto k32c) {
+    constexpr bool K32 = decltype(k32c)::value;
+    using key_t = typename std::conditional<K32, uint32_t, uint64_t>::type;
+    constexpr key_t KMAX = static_cast<key_t>(~0ull);
     const bool phase1 = n_wait > free_total;
     int cp[WPL];
     long long F0[WPL];
@@ -648,29 +720,30 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       F0[j] = g < G ? A[j] + d * k * n[j] : 0;
       if (g < G) s_capb[g] = cp[j];
     }
-    auto lane_key = [&](const long long* ld, const int* fr) -> uint64_t {
-      uint64_t best = ~0ull;
+    auto lane_key = [&](const long long* ld, const int* fr) -> key_t {
+      key_t best = KMAX;
 #pragma unroll
       for (int j = 0; j < WPL; ++j) {
-        int g = lane + 32 * j;
-        if (g < G && fr[j] > 0) {
-          uint64_t kk = (static_cast<uint64_t>(ld[j]) << gbits) | static_cast<uint64_t>(g);
-          best = kk < best ? kk : best;
-        }
+        const int g = lane + 32 * j;
+        const key_t kk = (static_cast<key_t>(ld[j]) << gbits) | static_cast<key_t>(g);
+        best = (fr[j] > 0 && kk < best) ? kk : best;  // fr == 0 for g >= G
       }
       return best;
     };
-    auto warp_argmin = [&](uint64_t key) -> uint64_t {
-      if (k32) {
-        uint32_t r = __reduce_min_sync(FULLMASK, key == ~0ull ? 0xFFFFFFFFu : static_cast<uint32_t>(key));
-        return r == 0xFFFFFFFFu ? ~0ull : static_cast<uint64_t>(r);
-      }
-      return wmin_u64(key);
+    auto wmin = [&](key_t key) -> key_t {
+      if constexpr (K32) return __reduce_min_sync(FULLMASK, key);
+      else return wmin_u64(key);
     };
-    __syncwarp();
+    // prefetch one deque entry into the stage (async; waited before resolution)
+    auto fetch = [&](int slot, int base, int idx) {
+      if constexpr (SM) cp_async8(&stage[slot], &deq[base + idx]);
+      else stage[slot] = deq[base + idx];
+    };
 
     if (phase1) {
-      // water filling (policies.hpp:274-323) restated over class deques (F4)
+      // water filling (policies.hpp:274-323) restated over class deques (F4):
+      // the lowest-loaded worker with a free slot takes the latest request of
+      // the largest class <= deficit, else the earliest of the smallest class.
       long long ld[WPL];
       int fr[WPL];
       long long tmax = 0;
@@ -682,36 +755,29 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       }
       long long target = static_cast<long long>(
           __reduce_max_sync(FULLMASK, static_cast<uint32_t>(tmax)));
-      uint64_t lk = lane_key(ld, fr);
+      key_t lk = lane_key(ld, fr);
       for (int q = 0; q < U; ++q) {
-        uint64_t km = warp_argmin(lk);
-        long long lmin = static_cast<long long>(km >> gbits);
-        int gs = static_cast<int>(km & gmask);
-        long long deficit = target - lmin;
-        int c = wset.highest_le(deficit);
-        bool back = c != 0;
+        const key_t km = wmin(lk);
+        const long long lmin = static_cast<long long>(km >> gbits);
+        const int gs = static_cast<int>(km) & static_cast<int>(gmask);
+        int c = wset.highest_le(target - lmin);
+        const bool back = c != 0;
         if (!back) c = wset.lowest();
-        int fnt = c_front[c], bck = c_back[c];
-        int t = c_pc[c];
-        int idx;
-        if (back) {
-          --bck;
-          idx = bck;
-        } else {
-          idx = fnt;
-          ++fnt;
-        }
-        __syncwarp();
+        // one 128-bit record load; every lane stores the same updated record
+        int4 cr = c_rec[c];
+        const int idx = back ? cr.y - 1 : cr.x;
+        const int t = cr.z;
+        if (cr.y - cr.x == 1) wset.clear(c);
+        if (back) cr.y -= 1;
+        else cr.x += 1;
+        cr.z = t + 1;
+        c_rec[c] = cr;
         if (lane == 0) {
-          if (back) c_back[c] = bck;
-          else c_front[c] = fnt;
-          c_pc[c] = t + 1;
-          p_idx[q] = cbase[c] + idx;
           p_cl[q] = c;
           p_t[q] = t;
+          fetch(q, cr.w, idx);
         }
-        if (fnt == bck) wset.clear(c);
-        if (t == 0) pset.add_uniform(c);
+        pset.add_uniform(c);
 #pragma unroll
         for (int j = 0; j < WPL; ++j)
           if (lane + 32 * j == gs) {
@@ -719,9 +785,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
             fr[j] -= 1;
           }
         lk = lane_key(ld, fr);
-        long long nl = lmin + c;
+        const long long nl = lmin + c;
         target = nl > target ? nl : target;
-        __syncwarp();
       }
     }
 
@@ -733,58 +798,53 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     if (H == 0) {
       // placement (policies.hpp:339-367) at H = 0: argmin (load, index) over
       // workers with a free slot (F3), items in w0-descending class order
-      uint64_t lk = lane_key(F0, cp);
+      key_t lk = lane_key(F0, cp);
       int jpos = 0;
       ClassSet<SMALLC>& set = phase1 ? pset : wset;
       while (!set.empty()) {
-        int c = set.highest();
-        int nc, f0 = 0;
+        const int c = set.highest();
+        int4 cr = c_rec[c];
+        int nc;
         if (phase1) {
-          nc = c_pc[c];
+          nc = cr.z;
+          cr.z = 0;
         } else {
-          f0 = c_front[c];
-          nc = c_back[c] - f0;
-        }
-        __syncwarp();
-        if (lane == 0) {
-          if (phase1) {
-            c_cs[c] = jpos;
-            c_pc[c] = 0;
-          } else {
-            c_front[c] = c_back[c];
+          nc = cr.y - cr.x;
+          for (int t = lane; t < nc; t += 32) {
+            p_cl[jpos + t] = c;
+            fetch(jpos + t, cr.w, cr.x + t);
           }
+          cr.x = cr.y;
         }
+        c_rec[c] = cr;
+        c_cs[c] = jpos;
         set.clear(c);
-        for (int t = 0; t < nc; ++t) {
-          uint64_t km = warp_argmin(lk);
-          int gs = static_cast<int>(km & gmask);
+        const long long inc = c + ak;
+        for (int t = 0; t < nc; ++t, ++jpos) {
+          const key_t km = wmin(lk);
+          const int gs = static_cast<int>(km) & static_cast<int>(gmask);
 #pragma unroll
           for (int j = 0; j < WPL; ++j)
             if (lane + 32 * j == gs) {
               F0[j] += c;
               cp[j] -= 1;
-              A[j] += c + ak;
+              A[j] += inc;
               s_res[jpos] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
               adm[j] += 1;
             }
-          if (!phase1 && lane == 0) {
-            p_idx[jpos] = cbase[c] + f0 + t;
-            p_cl[jpos] = c;
-          }
           lk = lane_key(F0, cp);
-          ++jpos;
         }
       }
+      if (SM) cp_async_wait_all();
       __syncwarp();
       for (int q = lane; q < U; q += 32) {
-        int c = p_cl[q];
-        uint32_t r = s_res[phase1 ? c_cs[c] + p_t[q] : q];
-        int2 e = deq[p_idx[q]];
+        const int c = p_cl[q];
+        const uint32_t r = s_res[phase1 ? c_cs[c] + p_t[q] : q];
+        const int2 e = stage[q];
         place(static_cast<int>(r & 0xFFFFu), static_cast<int>(r >> 16), e.x, c, e.y);
       }
     } else {
       // general H: lookahead views F_h[g] from the finish window
-      const int H1 = H + 1;
 #pragma unroll
       for (int j = 0; j < WPL; ++j) {
         int g = lane + 32 * j;
@@ -803,52 +863,44 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
           s_F[h * G + g] = F;
         }
       }
+      // ordered items: w0 descending, ties in pick order (phase 1) or waiting order
+      int jpos = 0;
+      ClassSet<SMALLC>& set = phase1 ? pset : wset;
+      while (!set.empty()) {
+        const int c = set.highest();
+        int4 cr = c_rec[c];
+        int nc;
+        if (phase1) {
+          nc = cr.z;
+          cr.z = 0;
+        } else {
+          nc = cr.y - cr.x;
+          for (int t = lane; t < nc; t += 32) {
+            p_cl[jpos + t] = c;
+            fetch(jpos + t, cr.w, cr.x + t);
+          }
+          cr.x = cr.y;
+        }
+        c_rec[c] = cr;
+        c_cs[c] = jpos;
+        set.clear(c);
+        jpos += nc;
+      }
+      if (SM) cp_async_wait_all();
       __syncwarp();
+      for (int q = lane; q < U; q += 32) {
+        const int c = p_cl[q];
+        const int jp = phase1 ? c_cs[c] + p_t[q] : q;
+        const int2 e = stage[q];
+        o_c[jp] = c;
+        o_o[jp] = e.y;
+        o_id[jp] = e.x;
+      }
       for (int h = lane; h <= H; h += 32) {
         long long m = 0;
         for (int g = 0; g < G; ++g) m = s_F[h * G + g] > m ? s_F[h * G + g] : m;
         s_M[h] = m;
       }
-      // ordered items: w0 descending, ties in pick order (phase 1) or waiting order
-      int jpos = 0;
-      ClassSet<SMALLC>& set = phase1 ? pset : wset;
-      while (!set.empty()) {
-        int c = set.highest();
-        int nc, f0 = 0;
-        if (phase1) {
-          nc = c_pc[c];
-        } else {
-          f0 = c_front[c];
-          nc = c_back[c] - f0;
-          for (int t = lane; t < nc; t += 32) {
-            int2 e = deq[cbase[c] + f0 + t];
-            o_c[jpos + t] = c;
-            o_o[jpos + t] = e.y;
-            o_id[jpos + t] = e.x;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          if (phase1) {
-            c_cs[c] = jpos;
-            c_pc[c] = 0;
-          } else {
-            c_front[c] = c_back[c];
-          }
-        }
-        set.clear(c);
-        jpos += nc;
-      }
-      __syncwarp();
-      if (phase1)
-        for (int q = lane; q < U; q += 32) {
-          int c = p_cl[q];
-          int jp = c_cs[c] + p_t[q];
-          int2 e = deq[p_idx[q]];
-          o_c[jp] = c;
-          o_o[jp] = e.y;
-          o_id[jp] = e.x;
-        }
       __syncwarp();
       for (int q = 0; q < U; ++q) {
         const int c = o_c[q], o = o_o[q];
@@ -899,7 +951,6 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         uint32_t r = s_res[q];
         place(static_cast<int>(r & 0xFFFFu), static_cast<int>(r >> 16), o_id[q], o_c[q], o_o[q]);
       }
-      (void)H1;
     }
 #pragma unroll
     for (int j = 0; j < WPL; ++j) n[j] += adm[j];
@@ -907,44 +958,82 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   };
 
   // ---- retire requests finishing at step k (+ window entry at k + H) ----
+  // All 32 lanes scan the finish-step array with 128-bit shared loads and
+  // append matches to per-worker lists (32-bit shared atomics); each owner lane
+  // then retires its workers' requests in registers.
   auto retire = [&]() {
-    long long nd = 0;
-    double tp = 0.0;
     const uint32_t kf = static_cast<uint32_t>(k);
-    const uint32_t kh = static_cast<uint32_t>(k + H);
+    const uint32_t kh = (GREEDY && H > 0) ? static_cast<uint32_t>(k + H) : kf;
     const int rk = static_cast<int>(k % Hm);
+    if (GREEDY && H > 0) {
 #pragma unroll
-    for (int j = 0; j < WPL; ++j) {
-      int g = lane + 32 * j;
-      if (g >= G) continue;
-      if (GREEDY && H > 0) {
-        s_Wc[rk * G + g] = 0;
-        s_Wa[rk * G + g] = 0;
+      for (int j = 0; j < WPL; ++j) {
+        int g = lane + 32 * j;
+        if (g < G) {
+          s_Wc[rk * G + g] = 0;
+          s_Wa[rk * G + g] = 0;
+        }
       }
-      if (n[j] == 0) continue;
-      const int base = g * B;
-      for (int i = 0; i < B; ++i) {
-        uint32_t f = s_f[base + i];
-        if (f == kf) {
-          int slot = base + i;
-          int x = s_x[slot];
-          A[j] -= s_a[slot];
-          int cap = B - n[j];
-          s_stk[base + cap] = static_cast<uint16_t>(i);
-          n[j] -= 1;
-          s_f[slot] = kEmpty;
-          // (finish - admit) / o per completed request (metrics.hpp:43-53)
-          double admit = ring[x & Rm];
-          tp = __dadd_rn(tp, __ddiv_rn(__dsub_rn(clock, admit), static_cast<double>(k - x + 1)));
-          ++nd;
-          if (emit_reqs) P.reqs.finish_clock[ro + s_id[slot]] = clock;
-        } else if (GREEDY && H > 0 && f == kh) {
-          s_Wc[rk * G + g] += 1;
-          s_Wa[rk * G + g] += s_a[base + i];
+      __syncwarp();
+    }
+    const int nslot4 = (G * B + 3) >> 2;
+    const uint4* f4 = reinterpret_cast<const uint4*>(s_f);
+    for (int q = lane; q < nslot4; q += 32) {
+      const uint4 v = f4[q];
+      uint32_t m = (v.x == kf ? 1u : 0u) | (v.y == kf ? 2u : 0u) | (v.z == kf ? 4u : 0u) |
+                   (v.w == kf ? 8u : 0u);
+      uint32_t me = 0;
+      if (GREEDY && H > 0)
+        me = (v.x == kh ? 1u : 0u) | (v.y == kh ? 2u : 0u) | (v.z == kh ? 4u : 0u) |
+             (v.w == kh ? 8u : 0u);
+      while (m | me) {
+        const int c = __ffs(m | me) - 1;
+        const bool fin = (m >> c) & 1u;
+        m &= ~(1u << c);
+        me &= ~(1u << c);
+        const int slot = 4 * q + c;
+        int g = static_cast<int>(static_cast<float>(slot) * invB);
+        g -= (g * B > slot) ? 1 : 0;
+        g += ((g + 1) * B <= slot) ? 1 : 0;
+        if (fin) {
+          const int pos = atomicAdd(&s_rn[g], 1);
+          s_rlist[g * B + pos] = static_cast<uint16_t>(slot - g * B);
+        } else {  // enters the lookahead window [k+1, k+H]
+          atomicAdd(&s_Wc[rk * G + g], 1);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&s_Wa[rk * G + g]),
+                    static_cast<unsigned long long>(static_cast<long long>(s_a[slot])));
         }
       }
     }
-    long long ndw = wsum_i64(nd);
+    __syncwarp();
+    long long nd = 0;
+    double tp = 0.0;
+#pragma unroll
+    for (int j = 0; j < WPL; ++j) {
+      const int g = lane + 32 * j;
+      if (g >= G) continue;
+      const int nr = s_rn[g];
+      if (nr == 0) continue;
+      s_rn[g] = 0;
+      int cap = B - n[j];
+      for (int e = 0; e < nr; ++e) {
+        const int i = s_rlist[g * B + e];
+        const int slot = g * B + i;
+        const int x = s_x[slot];
+        A[j] -= s_a[slot];
+        s_stk[g * B + cap] = static_cast<uint16_t>(i);
+        ++cap;
+        s_f[slot] = kEmpty;
+        // (finish - admit) / o per completed request (metrics.hpp:43-53)
+        const double admit = ring[x & Rm];
+        tp = __dadd_rn(tp, __ddiv_rn(__dsub_rn(clock, admit), static_cast<double>(k - x + 1)));
+        if (emit_reqs) P.reqs.finish_clock[ro + s_id[slot]] = clock;
+      }
+      n[j] -= nr;
+      nd += nr;
+      s_cap[g] = cap;
+    }
+    const long long ndw = wsum_i64(nd);
     done += ndw;
     act -= ndw;
     tpot_sum = __dadd_rn(tpot_sum, wsum_f64(tp));
@@ -973,12 +1062,21 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     const long long free_total = static_cast<long long>(G) * B - act;
     if (n_wait > 0 && free_total > 0) {
       int U = static_cast<int>(n_wait < free_total ? n_wait : free_total);
-      if constexpr (GREEDY) admit_greedy(U, free_total);
-      else admit_fifo(U);
+      if constexpr (GREEDY) {
+        if (k32) admit_greedy(U, free_total, std::true_type{});
+        else admit_greedy(U, free_total, std::false_type{});
+      } else {
+        admit_fifo(U);
+      }
       n_wait -= U;
       act += U;
       adm_total += U;
       if (OVL) refresh_maxcount();
+#pragma unroll
+      for (int j = 0; j < WPL; ++j) {
+        int g = lane + 32 * j;
+        if (g < G) s_cap[g] = B - n[j];
+      }
     }
     // loads, straggler max, dt, clock (engine.hpp:136-146)
     uint32_t lmax = 0;
@@ -1006,7 +1104,9 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     if (kr == 31) flush(k - 31, 32);
     if (act > 0 || (GREEDY && H > 0)) retire();
     ++k;
+    prefetch_fifo();
   }
+  if (SM) cp_async_wait_all();
   if (k & 31) flush(k & ~31ll, static_cast<int>(k & 31));
 
   // unrevealed requests (partial runs)
@@ -1054,28 +1154,26 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   __syncwarp();
 }
 
-template <int MODE, int POL, int WPL, bool SMALLC>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
-    step_kernel(KParams P) {
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) step_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
   unsigned char* sm = smem + static_cast<size_t>(warp) * P.plan.smem_per_warp;
-  unsigned char* ws =
-      P.ws + static_cast<size_t>(blockIdx.x * wpc + warp) * P.plan.ws_stride;
+  unsigned char* ws = P.ws + static_cast<size_t>(blockIdx.x * wpc + warp) * P.plan.ws_stride;
   for (;;) {
     int qi = 0;
     if (lane == 0) qi = atomicAdd(P.queue, 1);
     qi = __shfl_sync(FULLMASK, qi, 0);
     if (qi >= P.n) break;
-    run_traj<MODE, POL, WPL, SMALLC>(P, P.order[qi], sm, ws);
+    run_traj<MODE, POL, WPL, SMALLC, SM>(P, P.order[qi], sm, ws);
   }
 }
 
-template <int MODE, int POL, int WPL, bool SMALLC>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM>
 int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
-  auto fn = step_kernel<MODE, POL, WPL, SMALLC>;
+  auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM>;
   size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * wpc;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -1088,34 +1186,34 @@ int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
   return static_cast<int>(cudaGetLastError());
 }
 
-// Only bfio-greedy uses the class bitmaps, so the FIFO families ignore `small`.
-template <int MODE, int POL>
-int launch_family(int wpl, int small, const KParams& kp, int grid, int wpc, cudaStream_t s,
-                  int* occ) {
-  constexpr bool kClasses = POL == BFSIM_POLICY_BFIO_GREEDY;
-  if (kClasses && !small) {
-    switch (wpl) {
-      case 1: return launch_t<MODE, POL, 1, false>(kp, grid, wpc, s, occ);
-      case 2: return launch_t<MODE, POL, 2, false>(kp, grid, wpc, s, occ);
-      case 4: return launch_t<MODE, POL, 4, false>(kp, grid, wpc, s, occ);
-      case 8: return launch_t<MODE, POL, 8, false>(kp, grid, wpc, s, occ);
-    }
-    return static_cast<int>(cudaErrorInvalidValue);
-  }
+template <int MODE, int POL, bool SMALLC, bool SM>
+int launch_w(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
   switch (wpl) {
-    case 1: return launch_t<MODE, POL, 1, true>(kp, grid, wpc, s, occ);
-    case 2: return launch_t<MODE, POL, 2, true>(kp, grid, wpc, s, occ);
-    case 4: return launch_t<MODE, POL, 4, true>(kp, grid, wpc, s, occ);
-    case 8: return launch_t<MODE, POL, 8, true>(kp, grid, wpc, s, occ);
+    case 1: return launch_t<MODE, POL, 1, SMALLC, SM>(kp, grid, wpc, s, occ);
+    case 2: return launch_t<MODE, POL, 2, SMALLC, SM>(kp, grid, wpc, s, occ);
+    case 4: return launch_t<MODE, POL, 4, SMALLC, SM>(kp, grid, wpc, s, occ);
+    case 8: return launch_t<MODE, POL, 8, SMALLC, SM>(kp, grid, wpc, s, occ);
   }
   return static_cast<int>(cudaErrorInvalidValue);
+}
+
+// Only bfio-greedy uses the class bitmaps, so the FIFO families ignore `small`.
+template <int MODE, int POL>
+int launch_family(int wpl, int small, int all_smem, const KParams& kp, int grid, int wpc,
+                  cudaStream_t s, int* occ) {
+  constexpr bool kClasses = POL == BFSIM_POLICY_BFIO_GREEDY;
+  if (kClasses && !small)
+    return all_smem ? launch_w<MODE, POL, false, true>(wpl, kp, grid, wpc, s, occ)
+                    : launch_w<MODE, POL, false, false>(wpl, kp, grid, wpc, s, occ);
+  return all_smem ? launch_w<MODE, POL, true, true>(wpl, kp, grid, wpc, s, occ)
+                  : launch_w<MODE, POL, true, false>(wpl, kp, grid, wpc, s, occ);
 }
 
 }  // namespace detail
 
 #define BFSIM_DECLARE_FAMILY(M, P)                                                            \
-  int launch_family_##M##_##P(int wpl, int small, const KParams& kp, int grid, int wpc,       \
-                              cudaStream_t s, int* occ);
+  int launch_family_##M##_##P(int wpl, int small, int all_smem, const KParams& kp, int grid,  \
+                              int wpc, cudaStream_t s, int* occ);
 BFSIM_DECLARE_FAMILY(0, 0)
 BFSIM_DECLARE_FAMILY(0, 1)
 BFSIM_DECLARE_FAMILY(0, 3)

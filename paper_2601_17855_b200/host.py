@@ -172,7 +172,17 @@ class Context:
 
     def run_batch(self, scen, pool: InputPool, *, emit_steps=False, emit_requests=False,
                   step_capacity=None):
-        """Host-pointer entry (the end-to-end path). Returns a BatchResult."""
+        """Host-pointer entry (the end-to-end path). Returns a BatchResult.
+        Step sinks are sized by a heuristic; if any scenario overflows it the
+        batch is re-run once with the exact step counts."""
+        br = self._run_batch(scen, pool, emit_steps=emit_steps, emit_requests=emit_requests,
+                             step_capacity=step_capacity)
+        if emit_steps and (br.res["flags"] & abi.FLAG_STEP_OVERFLOW).any():
+            br = self._run_batch(scen, pool, emit_steps=emit_steps, emit_requests=emit_requests,
+                                 step_capacity=np.maximum(br.res["steps_run"], 1))
+        return br
+
+    def _run_batch(self, scen, pool, *, emit_steps, emit_requests, step_capacity):
         L, err = lib(), _err()
         scen = np.array(scen, abi.scenario_dtype, copy=True).reshape(-1)
         n = scen.shape[0]
@@ -181,7 +191,7 @@ class Context:
         sink_s = sink_r = None
         nrec = nload = nreq = 0
         if emit_steps:
-            caps = np.array([_step_cap(s, pool, step_capacity) for s in scen], np.int64)
+            caps = _caps(scen, pool, step_capacity)
             scen["step_capacity"] = caps
             scen["step_offset"] = np.concatenate([[0], np.cumsum(caps)[:-1]])
             lcaps = caps * scen["workers"]
@@ -219,6 +229,12 @@ class _ReqSink(C.Structure):
     _fields_ = [("arrival_step", _vp), ("start_step", _vp), ("worker", _vp), ("admit_clock", _vp), ("finish_clock", _vp)]
 
 
+def _caps(scen, pool, step_capacity):
+    if step_capacity is not None and np.ndim(step_capacity) > 0:
+        return np.asarray(step_capacity, np.int64).reshape(-1).copy()
+    return np.array([_step_cap(s, pool, step_capacity) for s in scen], np.int64)
+
+
 def _step_cap(s, pool, explicit):
     if explicit is not None:
         return int(explicit)
@@ -232,7 +248,8 @@ def _step_cap(s, pool, explicit):
     work = int(np.asarray(recs["decode"], np.int64).sum())
     G, B = int(s["workers"]), int(s["batch"])
     span = float(recs["arrival_time"][-1]) / max(float(s["overhead"]), 1e-6)
-    bound = int(span) + work // max(1, G * B) + int(recs["decode"].max()) + 64 + work // 16
+    # heuristic capacity; run_batch re-runs any scenario that overflows it
+    bound = int(span) + (3 * work) // (2 * max(1, G * B)) + int(recs["decode"].max()) + 64
     return int(min(int(s["max_steps"]), bound))
 
 
@@ -271,3 +288,154 @@ def iir_reduce(fcfs_means, bfio_means):
     if rc:
         _raise(rc, err)
     return out
+
+
+class DeviceBatch:
+    """A scenario batch with inputs and output sinks resident in HBM (torch
+    tensors are only the allocator). run() enqueues the step kernels on the
+    current torch stream via bfsim_run_batch_device."""
+
+    def __init__(self, ctx: Context, scen, pool: InputPool, *, emit_steps=True, emit_requests=True,
+                 step_capacity=None):
+        import torch
+
+        self.ctx = ctx
+        dev = torch.device("cuda", ctx.device)
+        scen = np.array(scen, abi.scenario_dtype, copy=True).reshape(-1)
+        n = scen.shape[0]
+
+        def dbuf(arr):
+            t = torch.empty(max(1, arr.nbytes), dtype=torch.uint8, device=dev)
+            if arr.nbytes:
+                t[: arr.nbytes].copy_(torch.from_numpy(np.ascontiguousarray(arr).view(np.uint8).reshape(-1)))
+            return t
+
+        self._keep = []
+        self.records = dbuf(pool.records)
+        self.class_base = dbuf(pool.class_base)
+        self.is_stream = pool.kind == "stream"
+        self.pool = pool
+        self.steps = self.reqs = None
+        self.sink_s = self.sink_r = None
+        if emit_steps:
+            caps = _caps(scen, pool, step_capacity)
+            scen["step_capacity"] = caps
+            scen["step_offset"] = np.concatenate([[0], np.cumsum(caps)[:-1]])
+            lcaps = caps * scen["workers"]
+            scen["load_offset"] = np.concatenate([[0], np.cumsum(lcaps)[:-1]])
+            nrec, nload = int(caps.sum()), int(lcaps.sum())
+            self.steps = {
+                "clock_start": torch.empty(nrec, dtype=torch.float64, device=dev),
+                "dt": torch.empty(nrec, dtype=torch.float64, device=dev),
+                "max_load": torch.empty(nrec, dtype=torch.float64, device=dev),
+                "active_count": torch.empty(nrec, dtype=torch.int64, device=dev),
+                "loads": torch.empty(max(1, nload), dtype=torch.float64, device=dev),
+            }
+            self.sink_s = _StepSink(*[self.steps[k].data_ptr() for k in ("clock_start", "dt", "max_load", "active_count", "loads")])
+        if emit_requests:
+            lens = pool.inputs["length"][scen["input_id"]]
+            scen["req_offset"] = np.concatenate([[0], np.cumsum(lens)[:-1]])
+            nreq = int(lens.sum())
+            self.reqs = {
+                "arrival_step": torch.empty(nreq, dtype=torch.int32, device=dev),
+                "start_step": torch.empty(nreq, dtype=torch.int32, device=dev),
+                "worker": torch.empty(nreq, dtype=torch.int32, device=dev),
+                "admit_clock": torch.empty(nreq, dtype=torch.float64, device=dev),
+                "finish_clock": torch.empty(nreq, dtype=torch.float64, device=dev),
+            }
+            self.sink_r = _ReqSink(*[self.reqs[k].data_ptr() for k in ("arrival_step", "start_step", "worker", "admit_clock", "finish_clock")])
+        self.scen = scen
+        self.results = torch.empty(n * abi.result_dtype.itemsize, dtype=torch.uint8, device=dev)
+
+    def run(self, stream=None):
+        import torch
+
+        L, err = lib(), _err()
+        s = stream if stream is not None else torch.cuda.current_stream(self.ctx.device)
+        rc = L.bfsim_run_batch_device(
+            self.ctx.h, abi.ptr(self.scen), self.scen.shape[0], abi.ptr(self.pool.inputs),
+            self.pool.inputs.shape[0], self.class_base.data_ptr(),
+            None if self.is_stream else self.records.data_ptr(),
+            self.records.data_ptr() if self.is_stream else None,
+            C.byref(self.sink_s) if self.sink_s else None,
+            C.byref(self.sink_r) if self.sink_r else None,
+            self.results.data_ptr(), C.c_void_p(s.cuda_stream), err, 1024,
+        )
+        if rc:
+            _raise(rc, err)
+
+    def result_array(self):
+        return self.results.cpu().numpy().view(abi.result_dtype)
+
+
+class PinnedBatch:
+    """End-to-end batch through the host-pointer entry bfsim_run_batch with
+    page-locked host buffers (inputs copied H2D and all outputs D2H inside
+    every call)."""
+
+    def __init__(self, ctx: Context, scen, pool: InputPool, *, step_capacity, emit_requests=True):
+        import torch
+
+        def pinned(n, dtype):
+            t = torch.empty(max(1, int(n) * np.dtype(dtype).itemsize), dtype=torch.uint8, pin_memory=True)
+            self._keep.append(t)
+            return t.numpy().view(dtype)[: int(n)]
+
+        self._keep = []
+        self.ctx = ctx
+        scen = np.array(scen, abi.scenario_dtype, copy=True).reshape(-1)
+        caps = np.asarray(step_capacity, np.int64).reshape(-1)
+        scen["step_capacity"] = caps
+        scen["step_offset"] = np.concatenate([[0], np.cumsum(caps)[:-1]])
+        lcaps = caps * scen["workers"]
+        scen["load_offset"] = np.concatenate([[0], np.cumsum(lcaps)[:-1]])
+        self.nrec, self.nload = int(caps.sum()), int(lcaps.sum())
+        lens = pool.inputs["length"][scen["input_id"]]
+        scen["req_offset"] = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        self.nreq = int(lens.sum()) if emit_requests else 0
+        self.scen = pinned(scen.shape[0], abi.scenario_dtype)
+        self.scen[:] = scen
+        self.inputs = pinned(pool.inputs.shape[0], abi.input_dtype)
+        self.inputs[:] = pool.inputs
+        self.class_base = pinned(pool.class_base.shape[0], np.int32)
+        self.class_base[:] = pool.class_base
+        self.is_stream = pool.kind == "stream"
+        self.records = pinned(pool.records.shape[0], pool.records.dtype)
+        self.records[:] = pool.records
+        self.steps = {k: pinned(self.nrec, np.float64) for k in ("clock_start", "dt", "max_load")}
+        self.steps["active_count"] = pinned(self.nrec, np.int64)
+        self.steps["loads"] = pinned(max(1, self.nload), np.float64)
+        self.sink_s = _StepSink(*[abi.ptr(self.steps[k]) for k in ("clock_start", "dt", "max_load", "active_count", "loads")])
+        self.sink_r = None
+        if emit_requests:
+            self.reqs = {k: pinned(self.nreq, np.int32) for k in ("arrival_step", "start_step", "worker")}
+            self.reqs.update({k: pinned(self.nreq, np.float64) for k in ("admit_clock", "finish_clock")})
+            self.sink_r = _ReqSink(*[abi.ptr(self.reqs[k]) for k in ("arrival_step", "start_step", "worker", "admit_clock", "finish_clock")])
+        self.results = pinned(scen.shape[0], abi.result_dtype)
+
+    @property
+    def h2d_bytes(self):
+        return int(self.records.nbytes + self.class_base.nbytes + self.scen.nbytes + self.inputs.nbytes)
+
+    @property
+    def d2h_bytes(self):
+        b = self.results.nbytes + sum(v.nbytes for v in self.steps.values())
+        if self.sink_r is not None:
+            b += sum(v.nbytes for v in self.reqs.values())
+        return int(b)
+
+    def run(self):
+        L, err = lib(), _err()
+        st = self.is_stream
+        rc = L.bfsim_run_batch(
+            self.ctx.h, abi.ptr(self.scen), self.scen.shape[0], abi.ptr(self.inputs), self.inputs.shape[0],
+            abi.ptr(self.class_base), self.class_base.shape[0],
+            None if st else abi.ptr(self.records), 0 if st else self.records.shape[0],
+            abi.ptr(self.records) if st else None, self.records.shape[0] if st else 0,
+            C.byref(self.sink_s), self.nrec, self.nload,
+            C.byref(self.sink_r) if self.sink_r is not None else None, self.nreq,
+            abi.ptr(self.results), err, 1024,
+        )
+        if rc not in (abi.OK, abi.PARTIAL):
+            _raise(rc, err)
+        return self.results
