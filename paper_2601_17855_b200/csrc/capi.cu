@@ -163,7 +163,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     max_len = std::max<int64_t>(max_len, in.length);
   }
   int R = 1;
-  while (R <= max_o) R <<= 1;
+  while (R <= max_o + 33) R <<= 1;  // admit clocks stay readable until the 32-step TPOT drain
   p.G = G;
   p.B = B;
   p.H = H;
@@ -207,13 +207,14 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_res, GB * 4});
     items.push_back({&p.o_pcl, GB * 4});
     items.push_back({&p.o_pt, GB * 4});
+    items.push_back({&p.o_oc, GB * 4});
     if (H > 0) {
-      items.push_back({&p.o_oc, GB * 4});
       items.push_back({&p.o_oo, GB * 4});
       items.push_back({&p.o_oid, GB * 4});
     }
   }
-  items.push_back({&p.o_ring, R * 8LL});
+  p.cbuf = static_cast<int>(std::min<int64_t>(GB + 512, 1 << 24));
+  items.push_back({&p.o_misc, 16});
   int64_t sm_off = 0, ws_off = 0;
   int spilled = 0;
   for (auto& it : items) {
@@ -228,13 +229,17 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     }
   }
   p.all_smem = spilled ? 0 : 1;
-  if (greedy) {  // per-class waiting deques: counting-sort layout over the input
-    int64_t b = ((max_len * 8) + 15) & ~15LL;
-    p.o_deq = -(ws_off + 1);
-    ws_off += b;
-  } else {
-    p.o_deq = -1;
-  }
+  // cold arrays: always in the global workspace (touched once per step or per
+  // completion, off the dependent chain): clock ring, TPOT completion buffer,
+  // per-class waiting deques (counting-sort layout over the input)
+  auto cold = [&](int64_t* code, int64_t bytes) {
+    *code = -(ws_off + 1);
+    ws_off += (bytes + 15) & ~15LL;
+  };
+  cold(&p.o_ring, R * 8LL);
+  cold(&p.o_cbuf, static_cast<int64_t>(p.cbuf) * 8);
+  if (greedy) cold(&p.o_deq, max_len * 8);
+  else p.o_deq = -1;
   p.smem_per_warp = static_cast<int>((sm_off + 15) & ~15LL);
   if (p.smem_per_warp == 0) p.smem_per_warp = 16;
   p.ws_stride = std::max<int64_t>(16, (ws_off + 255) & ~255LL);
@@ -362,9 +367,10 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     });
     // shared memory: up to 4 warps per CTA within the opt-in limit
     // shared-memory budget per trajectory: enough trajectories resident per SM
-    // to hold the whole group at once (latency-bound warps), the rest spills
-    // to the per-warp global workspace
-    int64_t per_sm = (static_cast<int64_t>(g.idx.size()) + ctx->sm_count - 1) / ctx->sm_count;
+    // to hold every group of the batch at once (the groups run concurrently
+    // and the warps are latency-bound); what does not fit spills to the
+    // per-warp global workspace (generic-addressing kernel variant)
+    int64_t per_sm = (n_scen + ctx->sm_count - 1) / ctx->sm_count;
     per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, 16));
     int budget = static_cast<int>(std::min<int64_t>(ctx->smem_optin - 1024,
                                                     (228 * 1024) / per_sm - 2048));

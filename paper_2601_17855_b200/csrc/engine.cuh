@@ -34,6 +34,9 @@ struct Plan {
   int64_t o_stage, o_pcl, o_pt, o_res;
   // lookahead window (H > 0)
   int64_t o_F, o_M, o_Wc, o_Wa, o_oc, o_oo, o_oid;
+  // TPOT completion buffer (cbuf entries) + misc counters
+  int64_t o_cbuf, o_misc;
+  int cbuf, reserved2;
 };
 
 struct KParams {

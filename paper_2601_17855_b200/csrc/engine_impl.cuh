@@ -95,6 +95,12 @@ __device__ __forceinline__ T* at(unsigned char* sm, unsigned char* ws, int64_t c
   }
 }
 
+// Cold arrays always live in the global workspace (code < 0).
+template <class T>
+__device__ __forceinline__ T* gat(unsigned char* ws, int64_t code) {
+  return reinterpret_cast<T*>(ws + (-code - 1));
+}
+
 // ---------------------------------------------------------------------------
 // Set of non-empty prefill classes c = 1..S (bit c-1). SMALL: S <= 64 in one
 // uniform register word. Otherwise a 3-level 64-ary bitmap (top word in a
@@ -123,6 +129,7 @@ struct ClassSet<true> {
     bits |= (static_cast<uint64_t>(hi) << 32) | lo;
   }
   __device__ void add_uniform(int c) { bits |= 1ull << (c - 1); }
+  __device__ void clear_all() { bits = 0; }
 };
 
 template <>
@@ -245,6 +252,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   const int rstride = (G & 1) ? G : G + 1;  // padded accounting-ring row (bank conflicts)
   const int umax = pl.umax;
   const float invB = 1.0f / static_cast<float>(B);
+  const int cbuf_cap = pl.cbuf;
 
   // --- arenas --------------------------------------------------------------
   uint32_t* s_f = at<SM, uint32_t>(sm, ws, pl.o_f);
@@ -261,13 +269,13 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   double* r_cs = at<SM, double>(sm, ws, pl.o_rcs);
   uint32_t* r_mx = at<SM, uint32_t>(sm, ws, pl.o_rmx);
   int32_t* r_ac = at<SM, int32_t>(sm, ws, pl.o_rac);
-  double* ring = at<SM, double>(sm, ws, pl.o_ring);
+  double* ring = gat<double>(ws, pl.o_ring);  // cold: global workspace (L1/L2)
   const int Rm = pl.R - 1;
   // per-class record {front, back, picks this step, deque base} + chain start
   int4* c_rec = at<SM, int4>(sm, ws, pl.o_cls);
   int32_t* c_cs = reinterpret_cast<int32_t*>(c_rec + (pl.S + 2));
   uint16_t* s_rlist = at<SM, uint16_t>(sm, ws, pl.o_rlist);
-  int2* deq = reinterpret_cast<int2*>(ws + (-pl.o_deq - 1));
+  int2* deq = gat<int2>(ws, pl.o_deq);
   int2* stage = at<SM, int2>(sm, ws, pl.o_stage);  // prefetched (id|s, o) records
   int32_t* p_cl = at<SM, int32_t>(sm, ws, pl.o_pcl);
   int32_t* p_t = at<SM, int32_t>(sm, ws, pl.o_pt);
@@ -281,6 +289,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* s_Wc = at<SM, int32_t>(sm, ws, pl.o_Wc);
   long long* s_Wa = at<SM, long long>(sm, ws, pl.o_Wa);
   int32_t* o_c = at<SM, int32_t>(sm, ws, pl.o_oc);
+  int2* cbuf = gat<int2>(ws, pl.o_cbuf);  // cold: completions (x, finish step) for TPOT
+  int32_t* s_misc = at<SM, int32_t>(sm, ws, pl.o_misc);  // [0] completion-buffer fill
   int32_t* o_o = at<SM, int32_t>(sm, ws, pl.o_oo);
   int32_t* o_id = at<SM, int32_t>(sm, ws, pl.o_oid);
 
@@ -294,6 +304,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     s_rn[i] = 0;
     s_asum[i] = 0;
   }
+  if (lane == 0) s_misc[0] = 0;
   constexpr bool kClasses = GREEDY || OVL;
   if (kClasses)
     for (int c = lane; c <= S + 1; c += 32) c_rec[c] = make_int4(0, 0, 0, GREEDY ? cbase_g[c] : 0);
@@ -352,8 +363,27 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     b4 = load_raw(32 + lane);
   }
 
+  // ---- TPOT terms of buffered completions (metrics.hpp:43-53): request
+  // admitted at x, finished at step f: (clock_start[f+1] - clock_start[x]) / o,
+  // both read from the clock ring (callers guarantee ring[f+1] is written).
+  auto drain_tpot = [&]() {
+    __syncwarp();
+    const int nb = s_misc[0];
+    double tp = 0.0;
+    for (int e = lane; e < nb; e += 32) {
+      const int2 v = cbuf[e];
+      const double fin = ring[(v.y + 1) & Rm], adm = ring[v.x & Rm];
+      tp = __dadd_rn(tp, __ddiv_rn(__dsub_rn(fin, adm), static_cast<double>(v.y - v.x + 1)));
+    }
+    tpot_sum = __dadd_rn(tpot_sum, wsum_f64(tp));
+    __syncwarp();
+    if (lane == 0) s_misc[0] = 0;
+    __syncwarp();
+  };
+
   // ---- per-step accounting flush: steps k0 .. k0+cnt-1 in ring rows 0..cnt-1
   auto flush = [&](long long k0, int cnt) {
+    drain_tpot();
     double dp = 0.0, dtl = 0.0;
     long long imb_l = 0, sum_l = 0, ac_l = 0;
     bool counted = false;
@@ -777,7 +807,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
           p_t[q] = t;
           fetch(q, cr.w, idx);
         }
-        pset.add_uniform(c);
+        if constexpr (!SMALLC) pset.add_uniform(c);
 #pragma unroll
         for (int j = 0; j < WPL; ++j)
           if (lane + 32 * j == gs) {
@@ -795,10 +825,46 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     for (int j = 0; j < WPL; ++j) adm[j] = 0;
     const long long ak = -d * k;  // a = s - d*x with x = k
 
-    if (H == 0) {
-      // placement (policies.hpp:339-367) at H = 0: argmin (load, index) over
-      // workers with a free slot (F3), items in w0-descending class order
-      key_t lk = lane_key(F0, cp);
+    // Order the U admitted items as the reference's stable sort by w0
+    // descending (policies.hpp:324-326): class descending; within a class pick
+    // order (phase 1) or waiting order. o_c[j] = class of the j-th item;
+    // c_cs[c] = first position of class c. Without phase 1 every waiting
+    // request is admitted: the deques are drained and their entries prefetched
+    // into stage[j].
+    if constexpr (SMALLC) {
+      int run = 0;
+      for (int base = S; base >= 1; base -= 32) {  // S <= 64: at most two rounds
+        const int c = base - lane;
+        int nc = 0;
+        int4 cr = make_int4(0, 0, 0, 0);
+        if (c >= 1) {
+          cr = c_rec[c];
+          nc = phase1 ? cr.z : cr.y - cr.x;
+        }
+        int incl = nc;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int v = __shfl_up_sync(FULLMASK, incl, off);
+          if (lane >= off) incl += v;
+        }
+        const int start = run + incl - nc;
+        run += __shfl_sync(FULLMASK, incl, 31);
+        if (nc > 0) {
+          c_cs[c] = start;
+          if (phase1) {
+            cr.z = 0;
+          } else {
+            for (int t = 0; t < nc; ++t) {
+              o_c[start + t] = c;
+              fetch(start + t, cr.w, cr.x + t);
+            }
+            cr.x = cr.y;
+          }
+          c_rec[c] = cr;
+        }
+      }
+      if (!phase1) wset.clear_all();
+    } else {
       int jpos = 0;
       ClassSet<SMALLC>& set = phase1 ? pset : wset;
       while (!set.empty()) {
@@ -811,7 +877,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         } else {
           nc = cr.y - cr.x;
           for (int t = lane; t < nc; t += 32) {
-            p_cl[jpos + t] = c;
+            o_c[jpos + t] = c;
             fetch(jpos + t, cr.w, cr.x + t);
           }
           cr.x = cr.y;
@@ -819,26 +885,42 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         c_rec[c] = cr;
         c_cs[c] = jpos;
         set.clear(c);
-        const long long inc = c + ak;
-        for (int t = 0; t < nc; ++t, ++jpos) {
-          const key_t km = wmin(lk);
-          const int gs = static_cast<int>(km) & static_cast<int>(gmask);
+        jpos += nc;
+      }
+    }
+    __syncwarp();
+    if (phase1)
+      for (int q = lane; q < U; q += 32) {
+        const int c = p_cl[q];
+        o_c[c_cs[c] + p_t[q]] = c;
+      }
+    __syncwarp();
+
+    if (H == 0) {
+      // placement (policies.hpp:339-367) at H = 0: argmin (load, index) over
+      // workers with a free slot (F3), one warp reduction per item
+      key_t lk = lane_key(F0, cp);
+      int cnext = o_c[0];
+      for (int j = 0; j < U; ++j) {
+        const int c = cnext;
+        if (j + 1 < U) cnext = o_c[j + 1];
+        const key_t km = wmin(lk);
+        const int gs = static_cast<int>(km) & static_cast<int>(gmask);
 #pragma unroll
-          for (int j = 0; j < WPL; ++j)
-            if (lane + 32 * j == gs) {
-              F0[j] += c;
-              cp[j] -= 1;
-              A[j] += inc;
-              s_res[jpos] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
-              adm[j] += 1;
-            }
-          lk = lane_key(F0, cp);
-        }
+        for (int jj = 0; jj < WPL; ++jj)
+          if (lane + 32 * jj == gs) {
+            F0[jj] += c;
+            cp[jj] -= 1;
+            A[jj] += c + ak;
+            s_res[j] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[jj]) << 16);
+            adm[jj] += 1;
+          }
+        lk = lane_key(F0, cp);
       }
       if (SM) cp_async_wait_all();
       __syncwarp();
       for (int q = lane; q < U; q += 32) {
-        const int c = p_cl[q];
+        const int c = phase1 ? p_cl[q] : o_c[q];
         const uint32_t r = s_res[phase1 ? c_cs[c] + p_t[q] : q];
         const int2 e = stage[q];
         place(static_cast<int>(r & 0xFFFFu), static_cast<int>(r >> 16), e.x, c, e.y);
@@ -863,36 +945,11 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
           s_F[h * G + g] = F;
         }
       }
-      // ordered items: w0 descending, ties in pick order (phase 1) or waiting order
-      int jpos = 0;
-      ClassSet<SMALLC>& set = phase1 ? pset : wset;
-      while (!set.empty()) {
-        const int c = set.highest();
-        int4 cr = c_rec[c];
-        int nc;
-        if (phase1) {
-          nc = cr.z;
-          cr.z = 0;
-        } else {
-          nc = cr.y - cr.x;
-          for (int t = lane; t < nc; t += 32) {
-            p_cl[jpos + t] = c;
-            fetch(jpos + t, cr.w, cr.x + t);
-          }
-          cr.x = cr.y;
-        }
-        c_rec[c] = cr;
-        c_cs[c] = jpos;
-        set.clear(c);
-        jpos += nc;
-      }
       if (SM) cp_async_wait_all();
       __syncwarp();
       for (int q = lane; q < U; q += 32) {
-        const int c = p_cl[q];
-        const int jp = phase1 ? c_cs[c] + p_t[q] : q;
+        const int jp = phase1 ? c_cs[p_cl[q]] + p_t[q] : q;
         const int2 e = stage[q];
-        o_c[jp] = c;
         o_o[jp] = e.y;
         o_id[jp] = e.x;
       }
@@ -958,9 +1015,10 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   };
 
   // ---- retire requests finishing at step k (+ window entry at k + H) ----
-  // All 32 lanes scan the finish-step array with 128-bit shared loads and
-  // append matches to per-worker lists (32-bit shared atomics); each owner lane
-  // then retires its workers' requests in registers.
+  // All 32 lanes scan the finish-step array with 128-bit shared loads (four
+  // independent loads in flight per lane) and append matches to per-worker
+  // lists; each owner lane then retires its workers' requests in registers.
+  // TPOT terms are buffered (x, k) and evaluated off the critical path.
   auto retire = [&]() {
     const uint32_t kf = static_cast<uint32_t>(k);
     const uint32_t kh = (GREEDY && H > 0) ? static_cast<uint32_t>(k + H) : kf;
@@ -978,14 +1036,11 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     }
     const int nslot4 = (G * B + 3) >> 2;
     const uint4* f4 = reinterpret_cast<const uint4*>(s_f);
-    for (int q = lane; q < nslot4; q += 32) {
-      const uint4 v = f4[q];
-      uint32_t m = (v.x == kf ? 1u : 0u) | (v.y == kf ? 2u : 0u) | (v.z == kf ? 4u : 0u) |
-                   (v.w == kf ? 8u : 0u);
-      uint32_t me = 0;
-      if (GREEDY && H > 0)
-        me = (v.x == kh ? 1u : 0u) | (v.y == kh ? 2u : 0u) | (v.z == kh ? 4u : 0u) |
-             (v.w == kh ? 8u : 0u);
+    auto match = [&](uint4 v, uint32_t key) -> uint32_t {
+      return (v.x == key ? 1u : 0u) | (v.y == key ? 2u : 0u) | (v.z == key ? 4u : 0u) |
+             (v.w == key ? 8u : 0u);
+    };
+    auto hit = [&](int q, uint32_t m, uint32_t me) {
       while (m | me) {
         const int c = __ffs(m | me) - 1;
         const bool fin = (m >> c) & 1u;
@@ -1004,10 +1059,31 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
                     static_cast<unsigned long long>(static_cast<long long>(s_a[slot])));
         }
       }
+    };
+    int q = lane;
+    for (; q + 96 < nslot4; q += 128) {
+      const uint4 v0 = f4[q], v1 = f4[q + 32], v2 = f4[q + 64], v3 = f4[q + 96];
+      const uint32_t m0 = match(v0, kf), m1 = match(v1, kf), m2 = match(v2, kf), m3 = match(v3, kf);
+      uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+      if (GREEDY && H > 0) {
+        e0 = match(v0, kh);
+        e1 = match(v1, kh);
+        e2 = match(v2, kh);
+        e3 = match(v3, kh);
+      }
+      if (m0 | m1 | m2 | m3 | e0 | e1 | e2 | e3) {
+        hit(q, m0, e0);
+        hit(q + 32, m1, e1);
+        hit(q + 64, m2, e2);
+        hit(q + 96, m3, e3);
+      }
+    }
+    for (; q < nslot4; q += 32) {
+      const uint4 v = f4[q];
+      hit(q, match(v, kf), (GREEDY && H > 0) ? match(v, kh) : 0u);
     }
     __syncwarp();
-    long long nd = 0;
-    double tp = 0.0;
+    int nd = 0;
 #pragma unroll
     for (int j = 0; j < WPL; ++j) {
       const int g = lane + 32 * j;
@@ -1016,27 +1092,24 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       if (nr == 0) continue;
       s_rn[g] = 0;
       int cap = B - n[j];
+      const int cb0 = atomicAdd(&s_misc[0], nr);
       for (int e = 0; e < nr; ++e) {
         const int i = s_rlist[g * B + e];
         const int slot = g * B + i;
-        const int x = s_x[slot];
         A[j] -= s_a[slot];
         s_stk[g * B + cap] = static_cast<uint16_t>(i);
         ++cap;
         s_f[slot] = kEmpty;
-        // (finish - admit) / o per completed request (metrics.hpp:43-53)
-        const double admit = ring[x & Rm];
-        tp = __dadd_rn(tp, __ddiv_rn(__dsub_rn(clock, admit), static_cast<double>(k - x + 1)));
+        cbuf[cb0 + e] = make_int2(s_x[slot], static_cast<int>(k));
         if (emit_reqs) P.reqs.finish_clock[ro + s_id[slot]] = clock;
       }
       n[j] -= nr;
       nd += nr;
       s_cap[g] = cap;
     }
-    const long long ndw = wsum_i64(nd);
+    const long long ndw = static_cast<long long>(__reduce_add_sync(FULLMASK, static_cast<unsigned>(nd)));
     done += ndw;
     act -= ndw;
-    tpot_sum = __dadd_rn(tpot_sum, wsum_f64(tp));
   };
 
   // --- step loop -----------------------------------------------------------
@@ -1101,13 +1174,20 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       ring[k & Rm] = cs;
     }
     __syncwarp();
-    if (kr == 31) flush(k - 31, 32);
+    if (kr == 31) {
+      flush(k - 31, 32);
+    } else if (s_misc[0] > cbuf_cap - G * B) {
+      drain_tpot();  // completion buffer nearly full: evaluate now (ring[k] is written)
+    }
     if (act > 0 || (GREEDY && H > 0)) retire();
     ++k;
     prefetch_fifo();
   }
   if (SM) cp_async_wait_all();
+  if (lane == 0) ring[k & Rm] = clock;  // clock_start of the (unsimulated) next step
+  __syncwarp();
   if (k & 31) flush(k & ~31ll, static_cast<int>(k & 31));
+  else drain_tpot();
 
   // unrevealed requests (partial runs)
   if (!OVL && emit_reqs)
