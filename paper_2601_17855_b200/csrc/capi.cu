@@ -105,7 +105,7 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
     return fail(err, errlen, BFSIM_EINVAL, "noisy lookahead is not yet supported on the GPU path");
   if (s.input_id < 0 || s.input_id >= n_inputs)
     return fail(err, errlen, BFSIM_EINVAL, "scenario: input_id out of range");
-  if (s.workers > 256) return fail(err, errlen, BFSIM_EINVAL, "GPU path: workers > 256 not supported yet");
+  if (s.workers > 1024) return fail(err, errlen, BFSIM_EINVAL, "GPU path: workers > 1024 not supported");
   if (s.batch > 65535) return fail(err, errlen, BFSIM_EINVAL, "GPU path: batch > 65535");
   if (static_cast<int64_t>(s.workers) * s.batch > (1 << 24))
     return fail(err, errlen, BFSIM_EINVAL, "GPU path: workers*batch too large");

@@ -35,6 +35,9 @@ namespace bfsim {
 namespace detail {
 
 #define FULLMASK 0xffffffffu
+// Loops over a lane's WPL workers: unrolled into registers up to 8 workers per
+// lane; above that (G > 256) the per-lane arrays live in L1-cached local memory.
+#define BFSIM_UNROLL_W _Pragma("unroll (WPL > 8 ? 1 : WPL)")
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -324,7 +327,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
 
   int n[WPL];
   long long A[WPL];
-#pragma unroll
+BFSIM_UNROLL_W
   for (int j = 0; j < WPL; ++j) {
     n[j] = 0;
     A[j] = 0;
@@ -616,7 +619,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   auto admit_fifo = [&](int U) {
     int cap0[WPL];
     int vext = JSQ ? INT_MAX : 0;
-#pragma unroll
+BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) {
       int g = lane + 32 * j;
       cap0[j] = g < G ? B - n[j] : 0;
@@ -631,7 +634,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       int v = static_cast<int>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(vext)));
       for (; v >= 1 && T < U; --v, ++nl) {
         int cnt = 0;
-#pragma unroll
+BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           unsigned mk = __ballot_sync(FULLMASK, cap0[j] >= v);
           cnt += __popc(mk);
@@ -651,7 +654,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       int v = static_cast<int>(__reduce_min_sync(FULLMASK, static_cast<uint32_t>(vext)));
       for (; v <= B - 1 && T < U; ++v, ++nl) {
         int cnt = 0;
-#pragma unroll
+BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           int g = lane + 32 * j;
           unsigned mk = __ballot_sync(FULLMASK, g < G && n[j] <= v);
@@ -675,7 +678,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       while (l + 1 < nl && lvT[l + 1] <= t) ++l;
       int pos = t - lvT[l];
       int g = 0;
-#pragma unroll
+BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         uint32_t mk = lvM[l * WPL + j];
         int c = __popc(mk);
@@ -707,7 +710,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       atomicAdd(&s_asum[g], static_cast<unsigned long long>(static_cast<long long>(s) - d * k));
     }
     __syncwarp();
-#pragma unroll
+BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) {
       int g = lane + 32 * j;
       if (g >= G) continue;
@@ -715,7 +718,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       for (int l = 0; l < nl; ++l) {
         int before = 0;
         bool mine = false;
-#pragma unroll
+BFSIM_UNROLL_W
         for (int j2 = 0; j2 < WPL; ++j2) {
           uint32_t mk = lvM[l * WPL + j2];
           if (j2 < j) before += __popc(mk);
@@ -743,7 +746,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     const bool phase1 = n_wait > free_total;
     int cp[WPL];
     long long F0[WPL];
-#pragma unroll
+BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) {
       int g = lane + 32 * j;
       cp[j] = g < G ? B - n[j] : 0;
@@ -752,7 +755,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     }
     auto lane_key = [&](const long long* ld, const int* fr) -> key_t {
       key_t best = KMAX;
-#pragma unroll
+BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         const int g = lane + 32 * j;
         const key_t kk = (static_cast<key_t>(ld[j]) << gbits) | static_cast<key_t>(g);
@@ -777,7 +780,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       long long ld[WPL];
       int fr[WPL];
       long long tmax = 0;
-#pragma unroll
+BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         ld[j] = F0[j];
         fr[j] = cp[j];
@@ -808,7 +811,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
           fetch(q, cr.w, idx);
         }
         if constexpr (!SMALLC) pset.add_uniform(c);
-#pragma unroll
+BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j)
           if (lane + 32 * j == gs) {
             ld[j] += c;
@@ -821,7 +824,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     }
 
     int adm[WPL];
-#pragma unroll
+BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) adm[j] = 0;
     const long long ak = -d * k;  // a = s - d*x with x = k
 
@@ -906,7 +909,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         if (j + 1 < U) cnext = o_c[j + 1];
         const key_t km = wmin(lk);
         const int gs = static_cast<int>(km) & static_cast<int>(gmask);
-#pragma unroll
+BFSIM_UNROLL_W
         for (int jj = 0; jj < WPL; ++jj)
           if (lane + 32 * jj == gs) {
             F0[jj] += c;
@@ -927,7 +930,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       }
     } else {
       // general H: lookahead views F_h[g] from the finish window
-#pragma unroll
+BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         int g = lane + 32 * j;
         if (g >= G) continue;
@@ -963,7 +966,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         const int c = o_c[q], o = o_o[q];
         // lane-best (cost, F0, g) over owned workers with a free slot
         uint64_t bc = ~0ull, bk = ~0ull;
-#pragma unroll
+BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           int g = lane + 32 * j;
           if (g >= G || cp[j] <= 0) continue;
@@ -983,7 +986,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         uint64_t cmin = wmin_u64(bc);
         uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
         int gs = static_cast<int>(kmin & gmask);
-#pragma unroll
+BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j)
           if (lane + 32 * j == gs) {
             for (int h = 0; h <= H; ++h) {
@@ -1009,7 +1012,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
         place(static_cast<int>(r & 0xFFFFu), static_cast<int>(r >> 16), o_id[q], o_c[q], o_o[q]);
       }
     }
-#pragma unroll
+BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) n[j] += adm[j];
     __syncwarp();
   };
@@ -1024,7 +1027,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     const uint32_t kh = (GREEDY && H > 0) ? static_cast<uint32_t>(k + H) : kf;
     const int rk = static_cast<int>(k % Hm);
     if (GREEDY && H > 0) {
-#pragma unroll
+BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         int g = lane + 32 * j;
         if (g < G) {
@@ -1084,7 +1087,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     }
     __syncwarp();
     int nd = 0;
-#pragma unroll
+BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) {
       const int g = lane + 32 * j;
       if (g >= G) continue;
@@ -1145,7 +1148,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
       act += U;
       adm_total += U;
       if (OVL) refresh_maxcount();
-#pragma unroll
+BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         int g = lane + 32 * j;
         if (g < G) s_cap[g] = B - n[j];
@@ -1154,7 +1157,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     // loads, straggler max, dt, clock (engine.hpp:136-146)
     uint32_t lmax = 0;
     const int kr = static_cast<int>(k & 31);
-#pragma unroll
+BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) {
       int g = lane + 32 * j;
       if (g < G) {
@@ -1273,6 +1276,8 @@ int launch_w(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int*
     case 2: return launch_t<MODE, POL, 2, SMALLC, SM>(kp, grid, wpc, s, occ);
     case 4: return launch_t<MODE, POL, 4, SMALLC, SM>(kp, grid, wpc, s, occ);
     case 8: return launch_t<MODE, POL, 8, SMALLC, SM>(kp, grid, wpc, s, occ);
+    case 16: return launch_t<MODE, POL, 16, SMALLC, SM>(kp, grid, wpc, s, occ);
+    case 32: return launch_t<MODE, POL, 32, SMALLC, SM>(kp, grid, wpc, s, occ);
   }
   return static_cast<int>(cudaErrorInvalidValue);
 }

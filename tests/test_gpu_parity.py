@@ -210,3 +210,25 @@ def test_rejections(ctx):
     with pytest.raises(host.InvalidArgument):
         ctx.run_batch(np.array([abi.scenario(mode=abi.OVERLOADED, steps=10, warmup=0)], abi.scenario_dtype),
                       host.InputPool([st]))
+
+
+def test_large_worker_counts(ctx, orc):
+    """G > 256 (32-worker-per-lane variant; BASELINE C4 sweeps G up to 1024)."""
+    scs, trs = [], []
+    for G, B, pol, H in ((300, 4, abi.BFIO_GREEDY, 0), (600, 2, abi.FCFS, 0), (1024, 2, abi.JSQ, 0),
+                         (1024, 1, abi.BFIO_GREEDY, 0), (513, 3, abi.BFIO_GREEDY, 3)):
+        scs.append(abi.scenario(policy=pol, workers=G, batch=B, horizon=H))
+        trs.append(host.sample_instance(G + B, rate=G * B * 2.5, duration=0.6, s_max=64, p=0.1))
+    br = _poisson_batch(ctx, scs, trs)
+    for i, (s, t) in enumerate(zip(br.scen, trs)):
+        check_poisson(orc, br, i, s, t)
+    # overloaded at G = 1024 (C4 shape, short)
+    stream = host.sample_stream(9, 200000, s_max=64, p=0.05)
+    so = [abi.scenario(mode=abi.OVERLOADED, policy=p, workers=1024, batch=4, steps=40, warmup=10, seed=9)
+          for p in (abi.FCFS, abi.BFIO_GREEDY)]
+    for s in so:
+        s["input_id"] = 0
+    br = ctx.run_batch(np.array(so, abi.scenario_dtype), host.InputPool([stream]), emit_steps=True,
+                       emit_requests=True)
+    for i in range(2):
+        _ovl_check(orc, br, i, br.scen[i], stream, 64)
