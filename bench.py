@@ -287,13 +287,18 @@ def run_ours(args):
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_evs)
     assert np.array_equal(r2["imb_total_i"], res["imb_total_i"])
 
-    # cross-rank: max time, total work; the final metric reduction over NCCL
+    # cross-rank: max time (device-timed), total work; the final metric
+    # reduction over NCCL (parallel.gather_results / allreduce_exact)
+    from paper_2601_17855_b200 import parallel
+
     t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
-    w = torch.tensor([worker_steps, int(res["imb_total_i"].sum()), int(res["total_workload_i"].sum())],
-                     dtype=torch.int64, device=dev)
+    w = torch.tensor([worker_steps], dtype=torch.int64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(w, op=dist.ReduceOp.SUM)
+    exact = parallel.allreduce_exact(res, device=dev)
+    allres = parallel.gather_results(res, rank * scen.shape[0], world * scen.shape[0], device=dev)
+    w = torch.tensor([int(w[0]), exact[0], exact[1]], dtype=torch.int64)
     ms_max, e2e_max = float(t[0]), float(t[1])
     total_ws = int(w[0]) * args.steps
     value = total_ws / (ms_max / 1e3)
@@ -330,7 +335,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": pb.d2h_bytes, "ms_per_step": e2e_max / args.steps},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
-            "imbalance_check": {"imb_total_i_sum": int(w[1]), "total_workload_i_sum": int(w[2])},
+            "imbalance_check": {"imb_total_i_sum": int(w[1]), "total_workload_i_sum": int(w[2]),
+                                "trajectories_gathered": int(allres.shape[0])},
         }
         print(json.dumps(line))
     if world > 1:
