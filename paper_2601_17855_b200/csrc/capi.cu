@@ -100,9 +100,8 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
   if (s.mode != BFSIM_MODE_POISSON && s.mode != BFSIM_MODE_OVERLOADED)
     return fail(err, errlen, BFSIM_EINVAL, "unknown mode");
   if (s.lookahead < 0 || s.lookahead > 2) return fail(err, errlen, BFSIM_EINVAL, "unknown lookahead");
-  if (s.lookahead == BFSIM_LOOKAHEAD_NOISY && s.policy == BFSIM_POLICY_BFIO_GREEDY &&
-      s.mode == BFSIM_MODE_POISSON && s.noise_sigma > 0.0)
-    return fail(err, errlen, BFSIM_EINVAL, "noisy lookahead is not yet supported on the GPU path");
+  if (s.lookahead == BFSIM_LOOKAHEAD_NOISY && !(s.noise_sigma >= 0.0 && s.noise_sigma < 1e300))
+    return fail(err, errlen, BFSIM_EINVAL, "noisy lookahead: bad noise_sigma");
   if (s.input_id < 0 || s.input_id >= n_inputs)
     return fail(err, errlen, BFSIM_EINVAL, "scenario: input_id out of range");
   if (s.workers > 1024) return fail(err, errlen, BFSIM_EINVAL, "GPU path: workers > 1024 not supported");
@@ -131,6 +130,18 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
   return BFSIM_OK;
 }
 
+// Noisy lookahead changes decisions only for bfio-greedy with a window
+// (H > 0) in the Poisson loop: FCFS/JSQ never read previews, entry h = 0 is
+// always exact, and run_overloaded always previews perfectly (oracle.hpp:185-199).
+// Elsewhere the draws the reference takes are unobservable.
+int noisy_variant(const bfsim_scenario_t& s) {
+  return s.lookahead == BFSIM_LOOKAHEAD_NOISY && s.noise_sigma > 0.0 &&
+                 s.policy == BFSIM_POLICY_BFIO_GREEDY && s.mode == BFSIM_MODE_POISSON &&
+                 s.horizon > 0
+             ? 1
+             : 0;
+}
+
 int wpl_for(int G) {
   int w = (G + 31) / 32;
   int p = 1;
@@ -139,7 +150,7 @@ int wpl_for(int G) {
 }
 
 struct Group {
-  int mode, policy, wpl, small;
+  int mode, policy, wpl, small, noisy;
   std::vector<int32_t> idx;
   Plan plan;
   int wpc = 4, grid = 0;
@@ -203,6 +214,12 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
   }
+  p.noisy = g.noisy;
+  if (g.noisy) {
+    items.push_back({&p.o_mt, 312 * 8});
+    items.push_back({&p.o_lst, GB * 2});
+    items.push_back({&p.o_onz, GB * 4});
+  }
   if (greedy) {
     items.push_back({&p.o_res, GB * 4});
     items.push_back({&p.o_pcl, GB * 4});
@@ -240,6 +257,12 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   cold(&p.o_cbuf, static_cast<int64_t>(p.cbuf) * 8);
   if (greedy) cold(&p.o_deq, max_len * 8);
   else p.o_deq = -1;
+  if (g.noisy) {
+    const int64_t words = (max_len + 63) / 64 + 2;
+    cold(&p.o_nzb, (GB + max_len) * 4);
+    cold(&p.o_abits, words * 8);
+    cold(&p.o_zpre, words * 4);
+  }
   p.smem_per_warp = static_cast<int>((sm_off + 15) & ~15LL);
   if (p.smem_per_warp == 0) p.smem_per_warp = 16;
   p.ws_stride = std::max<int64_t>(16, (ws_off + 255) & ~255LL);
@@ -340,18 +363,20 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
       return fail(err, errlen, BFSIM_EINVAL, "overloaded scenario without sample streams");
   }
   // group by kernel variant; LPT order inside a group
-  std::map<std::tuple<int, int, int, int>, Group> groups;
+  std::map<std::tuple<int, int, int, int, int>, Group> groups;
   for (int64_t i = 0; i < n_scen; ++i) {
     const auto& s = scen_host[i];
     const auto& in = inputs_host[s.input_id];
     int small = in.s_max <= 64 ? 1 : 0;
     int wpl = wpl_for(s.workers);
-    auto key = std::make_tuple(s.mode, s.policy, wpl, small);
+    int noisy = noisy_variant(s);
+    auto key = std::make_tuple(s.mode, s.policy, wpl, small, noisy);
     auto& g = groups[key];
     g.mode = s.mode;
     g.policy = s.policy;
     g.wpl = wpl;
     g.small = small;
+    g.noisy = noisy;
     g.idx.push_back(static_cast<int32_t>(i));
   }
   if (static_cast<int>(groups.size()) > kMaxGroups)
@@ -381,8 +406,8 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     KParams probe{};
     probe.plan = g.plan;
     int occ = 0;
-    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, probe, 0, g.wpc, nullptr,
-                                       &occ);
+    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, g.noisy, probe, 0, g.wpc,
+                                       nullptr, &occ);
     if (rc != 0 || occ <= 0)
       return fail(err, errlen, BFSIM_ECUDA, "step kernel does not fit on the device");
     int64_t warps_needed = static_cast<int64_t>(g.idx.size());
@@ -428,7 +453,8 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     kp.ws = static_cast<unsigned char*>(ctx->ws.p) + ws_off;
     kp.queue = static_cast<int32_t*>(ctx->queue.p) + gi;
     kp.plan = g.plan;
-    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, kp, g.grid, g.wpc, s, nullptr);
+    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, g.noisy, kp, g.grid, g.wpc,
+                                       s, nullptr);
     if (rc != 0) return cuda_fail(err, errlen, static_cast<cudaError_t>(rc), "step kernel launch");
     ++launches;
     if (gl.size() > 1) {

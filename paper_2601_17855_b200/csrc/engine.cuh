@@ -36,7 +36,10 @@ struct Plan {
   int64_t o_F, o_M, o_Wc, o_Wa, o_oc, o_oo, o_oid;
   // TPOT completion buffer (cbuf entries) + misc counters
   int64_t o_cbuf, o_misc;
-  int cbuf, reserved2;
+  // noisy lookahead: mt19937_64 state, per-worker active lists, per-item
+  // draws (hot); the step's draws, admitted-id bitmap and its word prefix (cold)
+  int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre;
+  int cbuf, noisy;
 };
 
 struct KParams {
@@ -57,7 +60,7 @@ struct KParams {
 
 // Launch one group (grid CTAs of wpc warps) or, when occupancy != NULL, only
 // query CTAs per SM. Returns cudaError_t as int.
-int launch_step_kernel(int mode, int policy, int wpl, int small_classes, const KParams& kp,
-                       int grid, int wpc, void* stream, int* occupancy);
+int launch_step_kernel(int mode, int policy, int wpl, int small_classes, int noisy,
+                       const KParams& kp, int grid, int wpc, void* stream, int* occupancy);
 
 }  // namespace bfsim

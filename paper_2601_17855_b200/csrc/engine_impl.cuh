@@ -86,6 +86,75 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// ---------------------------------------------------------------------------
+// libstdc++ std::mt19937_64 (bits/random.h parameters) and the draws
+// make_preview takes from it in Noisy mode (policies.hpp:74-76):
+// normal_distribution<double>(0, sigma) -- polar method, a fresh object per
+// call (random.tcc:1809-1844) -- over generate_canonical<double, 53>, which is
+// one engine call for a 64-bit engine (random.tcc:3349-3381). Every rounding
+// step is spelled out with _rn intrinsics so nothing is FMA-contracted
+// (the reference build: -ffp-contract=off).
+constexpr int kMtN = 312, kMtM = 156;
+constexpr uint64_t kMtA = 0xB5026F5AA96619E9ull;
+constexpr uint64_t kMtUpper = 0xFFFFFFFF80000000ull, kMtLower = 0x000000007FFFFFFFull;
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  y ^= y >> 43;
+  return y;
+}
+
+__device__ __forceinline__ uint64_t mt_mix(uint64_t lo_word, uint64_t next, uint64_t far) {
+  const uint64_t x = (lo_word & kMtUpper) | (next & kMtLower);
+  return far ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+}
+
+// mersenne_twister_engine::seed: a 311-step sequential recurrence (lane 0).
+__device__ __forceinline__ void mt_seed(uint64_t* mt, uint64_t seed) {
+  if ((threadIdx.x & 31) == 0) {
+    uint64_t x = seed;
+    mt[0] = x;
+    for (int i = 1; i < kMtN; ++i) {
+      x = 6364136223846793005ull * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
+      mt[i] = x;
+    }
+  }
+  __syncwarp();
+}
+
+// _M_gen_rand, warp-parallel. The sequential loop reads, for i < 156, only
+// words not yet rewritten (i+1, i+156); for 156 <= i < 311 the rewritten word
+// i-156 and the old word i+1; i = 311 reads the rewritten words 155 and 0.
+// So two parallel halves reproduce it exactly (reads of a 32-wide chunk are
+// fenced from its writes by __syncwarp).
+__device__ __forceinline__ void mt_twist(uint64_t* mt) {
+  const int lane = threadIdx.x & 31;
+  for (int b = 0; b < kMtM; b += 32) {
+    const int i = b + lane;
+    uint64_t v = 0;
+    if (i < kMtM) v = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
+    __syncwarp();
+    if (i < kMtM) mt[i] = v;
+    __syncwarp();
+  }
+  for (int b = kMtM; b < kMtN; b += 32) {
+    const int i = b + lane;
+    uint64_t v = 0;
+    if (i < kMtN) v = mt_mix(mt[i], mt[i + 1 < kMtN ? i + 1 : 0], mt[i - kMtM]);
+    __syncwarp();
+    if (i < kMtN) mt[i] = v;
+    __syncwarp();
+  }
+}
+
+// generate_canonical<double, 53>: (double)u / 2^64, clamped below 1.
+__device__ __forceinline__ double mt_canonical(uint64_t u) {
+  const double r = __dmul_rn(__ull2double_rn(u), 0x1p-64);
+  return r >= 1.0 ? 0x1.fffffffffffffp-1 : r;
+}
+
 // Array placement from the planner. SM: every code is a shared-memory offset,
 // so the compiler emits 32-bit shared loads/stores. Otherwise a code < 0 is
 // byte (-code - 1) of the warp's global workspace.
@@ -224,10 +293,11 @@ struct ClassSet<false> {
 
 // ---------------------------------------------------------------------------
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY>
 __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned char* ws) {
   constexpr bool OVL = MODE == BFSIM_MODE_OVERLOADED;
   constexpr bool GREEDY = POL == BFSIM_POLICY_BFIO_GREEDY;
+  static_assert(!NOISY || (GREEDY && !OVL), "noisy lookahead: Poisson bfio-greedy only");
   constexpr bool JSQ = POL == BFSIM_POLICY_JSQ;
   const Plan& pl = P.plan;
   const int lane = threadIdx.x & 31;
@@ -296,6 +366,16 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* s_misc = at<SM, int32_t>(sm, ws, pl.o_misc);  // [0] completion-buffer fill
   int32_t* o_o = at<SM, int32_t>(sm, ws, pl.o_oo);
   int32_t* o_id = at<SM, int32_t>(sm, ws, pl.o_oid);
+  // Noisy lookahead (NOISY): engine state, per-worker active lists in
+  // insertion order (interleaved [pos * G + g]), per-item draws, the step's
+  // draws and the admitted-id bitmap that gives waiting ranks.
+  uint64_t* s_mt = NOISY ? at<SM, uint64_t>(sm, ws, pl.o_mt) : nullptr;
+  uint16_t* s_lst = NOISY ? at<SM, uint16_t>(sm, ws, pl.o_lst) : nullptr;
+  int32_t* o_nz = NOISY ? at<SM, int32_t>(sm, ws, pl.o_onz) : nullptr;
+  int32_t* nzb = NOISY ? gat<int32_t>(ws, pl.o_nzb) : nullptr;
+  unsigned long long* abits = NOISY ? gat<unsigned long long>(ws, pl.o_abits) : nullptr;
+  int32_t* zpre = NOISY ? gat<int32_t>(ws, pl.o_zpre) : nullptr;
+  const double sigma = sc.noise_sigma;
 
   // --- init ----------------------------------------------------------------
   for (int i = lane; i < ((G * B + 3) & ~3); i += 32) {
@@ -322,6 +402,13 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     uint64_t* pbm = at<SM, uint64_t>(sm, ws, pl.o_pbm);
     wset.init(bm, bm + 64, S);
     pset.init(pbm, pbm + 64, S);
+  }
+  int mt_i = kMtN;       // next engine word in the current block (always even)
+  long long aw0 = 0;     // first bitmap word holding a waiting (revealed, unadmitted) id
+  bool ntie = false;     // a draw landed next to an lround tie (BFSIM_FLAG_NOISE_NEAR_TIE)
+  if constexpr (NOISY) {
+    mt_seed(s_mt, sc.seed);  // Simulation::rng_(config.seed), engine.hpp:97-98
+    for (long long w = lane; w < (N + 63) / 64 + 1; w += 32) abits[w] = 0ull;
   }
   __syncwarp();
 
@@ -598,6 +685,145 @@ BFSIM_UNROLL_W
       P.reqs.worker[ro + id] = g;
       P.reqs.admit_clock[ro + id] = clock;
     }
+  };
+
+  // ---- Noisy lookahead (NOISY) ------------------------------------------
+  // The D = active + waiting normal draws of one step, in the reference's
+  // order (engine.hpp:131 with GCC's right-to-left argument evaluation:
+  // worker_views -- g ascending, insertion order, engine.hpp:204-220 -- then
+  // waiting_views in waiting order, :222-231). Every polar attempt takes the
+  // two engine words at an even position, so lane l tests the pair at
+  // mt_i + 2l and accepted pairs are numbered by a ballot prefix. With
+  // `values`, draw r stores lround(N(0, sigma)) in nzb[r].
+  auto gen_normals = [&](long long D, bool values) {
+    long long got = 0;
+    while (got < D) {
+      if (mt_i >= kMtN) {
+        mt_twist(s_mt);
+        mt_i = 0;
+      }
+      const int pi = mt_i + 2 * lane;
+      const bool valid = pi < kMtN;
+      double y = 0.0, r2 = 0.0;
+      bool acc = false;
+      if (valid) {
+        const double u1 = mt_canonical(mt_temper(s_mt[pi]));
+        const double u2 = mt_canonical(mt_temper(s_mt[pi + 1]));
+        const double x = __dsub_rn(__dmul_rn(2.0, u1), 1.0);
+        y = __dsub_rn(__dmul_rn(2.0, u2), 1.0);
+        r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+        acc = !(r2 > 1.0 || r2 == 0.0);
+      }
+      const unsigned am = __ballot_sync(FULLMASK, acc);
+      const unsigned vm = __ballot_sync(FULLMASK, valid);
+      const long long need = D - got;
+      const long long r = got + __popc(am & lanemask_lt());
+      if (values && acc && r < D) {
+        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
+        const double nv = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), sigma), 0.0);
+        long long lr = llround(nv);
+        lr = lr > (1ll << 30) ? (1ll << 30) : (lr < -(1ll << 30) ? -(1ll << 30) : lr);
+        nzb[r] = static_cast<int32_t>(lr);
+        // CUDA log is within 1 ulp of glibc's; only a draw this close to a
+        // half-integer could round differently
+        const double av = fabs(nv);
+        if (fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
+      }
+      const int nacc = __popc(am);
+      if (nacc >= need) {
+        mt_i += 2 * (static_cast<int>(__fns(am, 0, static_cast<int>(need))) + 1);
+        got = D;
+      } else {
+        mt_i += 2 * __popc(vm);
+        got += nacc;
+      }
+    }
+    __syncwarp();
+  };
+
+  // Rank of each admitted request in the waiting order (arrival order of the
+  // revealed, unadmitted ids): zeros of the admitted-id bitmap below its id.
+  auto waiting_ranks = [&](int U, const int32_t* ids, int32_t* out) {
+    const long long wl = (nxt - 1) >> 6;
+    long long run = 0;
+    for (long long b = aw0; b <= wl; b += 32) {
+      const long long w = b + lane;
+      const int z = w <= wl ? 64 - __popcll(__ldcg(abits + w)) : 0;
+      int incl = z;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(FULLMASK, incl, off);
+        if (lane >= off) incl += v;
+      }
+      if (w <= wl) zpre[w - aw0] = static_cast<int32_t>(run + incl - z);
+      run += __shfl_sync(FULLMASK, incl, 31);
+    }
+    __syncwarp();
+    for (int q = lane; q < U; q += 32) {
+      const long long id = ids[q];
+      const unsigned long long below = (1ull << (id & 63)) - 1ull;
+      out[q] = zpre[(id >> 6) - aw0] + __popcll(~__ldcg(abits + (id >> 6)) & below);
+    }
+    __syncwarp();
+  };
+
+  // Lookahead views F_h[g] (worker_views, engine.hpp:204-220) from the
+  // per-slot draws: request i on g (finish step f, a = s - d*x) contributes
+  // w_i + d*h while h < min(c_i, rem_i) and its last workload a + d*f while
+  // rem_i <= h < c_i, c_i = min(max(1, rem_i + lround(n_i)), H + 1),
+  // rem_i = f - k + 1 (make_preview, policies.hpp:67-90). Owner lanes walk
+  // their workers' lists into difference arrays over h (s_Wa / s_Wc, unused
+  // by the noisy variant's retire) and prefix them into s_F.
+  auto noisy_views = [&]() {
+    long long base = 0;
+    int pre[WPL];
+BFSIM_UNROLL_W
+    for (int j = 0; j < WPL; ++j) {
+      const int v = lane + 32 * j < G ? n[j] : 0;
+      int incl = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(FULLMASK, incl, off);
+        if (lane >= off) incl += t;
+      }
+      pre[j] = static_cast<int>(base) + incl - v;
+      base += __shfl_sync(FULLMASK, incl, 31);
+    }
+BFSIM_UNROLL_W
+    for (int j = 0; j < WPL; ++j) {
+      const int g = lane + 32 * j;
+      if (g >= G) continue;
+      for (int p = 0; p < n[j]; ++p) {
+        const int slot = g * B + s_lst[p * G + g];
+        const long long f = s_f[slot];
+        const long long a = s_a[slot];
+        const long long rem = f - k + 1;
+        long long pred = rem + nzb[pre[j] + p];
+        pred = pred > 1 ? pred : 1;
+        const long long c = pred < H + 1 ? pred : H + 1;
+        const long long m = c < rem ? c : rem;
+        if (m <= H) {
+          s_Wa[(m - 1) * G + g] -= a + d * k;
+          s_Wc[(m - 1) * G + g] -= 1;
+        }
+        if (c > rem) {
+          const long long wl = a + d * f;
+          s_Wa[(rem - 1) * G + g] += wl;
+          if (c <= H) s_Wa[(c - 1) * G + g] -= wl;
+        }
+      }
+      long long SW = A[j] + d * k * n[j];
+      long long CN = n[j];
+      s_F[g] = SW;
+      for (int h = 1; h <= H; ++h) {
+        SW += s_Wa[(h - 1) * G + g];
+        CN += s_Wc[(h - 1) * G + g];
+        s_Wa[(h - 1) * G + g] = 0;
+        s_Wc[(h - 1) * G + g] = 0;
+        s_F[h * G + g] = SW + d * h * CN;
+      }
+    }
+    __syncwarp();
   };
 
   // FIFO policies: prefetch the (s, o) of the next step's oldest waiting
@@ -930,22 +1156,24 @@ BFSIM_UNROLL_W
       }
     } else {
       // general H: lookahead views F_h[g] from the finish window
+      if constexpr (!NOISY) {
 BFSIM_UNROLL_W
-      for (int j = 0; j < WPL; ++j) {
-        int g = lane + 32 * j;
-        if (g >= G) continue;
-        long long PA = 0, PC = 0, Q = 0;
-        for (int h = 0; h <= H; ++h) {
-          if (h > 0) {
-            int r = static_cast<int>((k + h - 1) % Hm);
-            PA += s_Wa[r * G + g];
-            PC += s_Wc[r * G + g];
-            Q += PC;
+        for (int j = 0; j < WPL; ++j) {
+          int g = lane + 32 * j;
+          if (g >= G) continue;
+          long long PA = 0, PC = 0, Q = 0;
+          for (int h = 0; h <= H; ++h) {
+            if (h > 0) {
+              int r = static_cast<int>((k + h - 1) % Hm);
+              PA += s_Wa[r * G + g];
+              PC += s_Wc[r * G + g];
+              Q += PC;
+            }
+            long long kh = k + h;
+            long long F = trunc ? A[j] + d * kh * n[j] - d * Q
+                                : (A[j] + d * kh * n[j]) - (PA + d * kh * PC);
+            s_F[h * G + g] = F;
           }
-          long long kh = k + h;
-          long long F = trunc ? A[j] + d * kh * n[j] - d * Q
-                              : (A[j] + d * kh * n[j]) - (PA + d * kh * PC);
-          s_F[h * G + g] = F;
         }
       }
       if (SM) cp_async_wait_all();
@@ -956,6 +1184,16 @@ BFSIM_UNROLL_W
         o_o[jp] = e.y;
         o_id[jp] = e.x;
       }
+      __syncwarp();
+      if constexpr (NOISY) {
+        // this step's draws (all of them, as the reference takes them), then
+        // the views from the active draws and each admitted request's own
+        // waiting draw
+        waiting_ranks(U, o_id, o_nz);
+        gen_normals(act + n_wait, true);
+        noisy_views();
+        for (int q = lane; q < U; q += 32) o_nz[q] = nzb[act + o_nz[q]];
+      }
       for (int h = lane; h <= H; h += 32) {
         long long m = 0;
         for (int g = 0; g < G; ++g) m = s_F[h * G + g] > m ? s_F[h * G + g] : m;
@@ -964,6 +1202,16 @@ BFSIM_UNROLL_W
       __syncwarp();
       for (int q = 0; q < U; ++q) {
         const int c = o_c[q], o = o_o[q];
+        // preview (make_preview, policies.hpp:67-90): w_h = c + d*min(h, o-1)
+        // for h < lim, else 0; lim = predicted completion (perfect: o;
+        // truncated: max(o, H+1); noisy: max(1, o + lround(n)))
+        long long lim = o;
+        if constexpr (NOISY) {
+          lim = static_cast<long long>(o) + o_nz[q];
+          lim = lim > 1 ? lim : 1;
+        } else {
+          if (trunc && lim < H + 1) lim = H + 1;
+        }
         // lane-best (cost, F0, g) over owned workers with a free slot
         uint64_t bc = ~0ull, bk = ~0ull;
 BFSIM_UNROLL_W
@@ -972,7 +1220,7 @@ BFSIM_UNROLL_W
           if (g >= G || cp[j] <= 0) continue;
           long long cost = 0;
           for (int h = 0; h <= H; ++h) {
-            long long w = h < o ? c + d * h : (trunc ? c + d * (o - 1) : 0);
+            long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
             long long v = s_F[h * G + g] + w;
             long long m = s_M[h];
             cost += v > m ? v : m;
@@ -990,7 +1238,7 @@ BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j)
           if (lane + 32 * j == gs) {
             for (int h = 0; h <= H; ++h) {
-              long long w = h < o ? c + d * h : (trunc ? c + d * (o - 1) : 0);
+              long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
               long long v = s_F[h * G + gs] + w;
               s_F[h * G + gs] = v;
               if (v > s_M[h]) s_M[h] = v;
@@ -999,7 +1247,7 @@ BFSIM_UNROLL_W
             A[j] += c + ak;
             s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
             adm[j] += 1;
-            if (o <= H) {  // finishes inside the window [k, k+H-1]
+            if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
               int r = static_cast<int>((k + o - 1) % Hm);
               s_Wc[r * G + gs] += 1;
               s_Wa[r * G + gs] += c + ak;
@@ -1010,6 +1258,44 @@ BFSIM_UNROLL_W
       for (int q = lane; q < U; q += 32) {
         uint32_t r = s_res[q];
         place(static_cast<int>(r & 0xFFFFu), static_cast<int>(r >> 16), o_id[q], o_c[q], o_o[q]);
+        if constexpr (NOISY) {
+          const long long id = o_id[q];
+          atomicOr(abits + (id >> 6), 1ull << (id & 63));
+        }
+      }
+      if constexpr (NOISY) {
+        // append this step's admissions to each worker's list in waiting
+        // order (Simulation::apply pushes in assignment order, sorted by
+        // waiting index: engine.hpp:233-248, policies.hpp:368)
+        __syncwarp();
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j) {
+          const int g = lane + 32 * j;
+          if (g >= G) continue;
+          const int capb = s_capb[g];
+          for (int t = 0; t < adm[j]; ++t) {
+            const int i = s_stk[g * B + capb - 1 - t];
+            const int key = s_id[g * B + i];
+            int pos = n[j] + t;
+            while (pos > n[j] && s_id[g * B + s_lst[(pos - 1) * G + g]] > key) {
+              s_lst[pos * G + g] = s_lst[(pos - 1) * G + g];
+              --pos;
+            }
+            s_lst[pos * G + g] = static_cast<uint16_t>(i);
+          }
+        }
+        // advance the first bitmap word that still holds a waiting id
+        const long long nw = (N + 63) / 64;
+        for (;;) {
+          const long long w = aw0 + lane;
+          const bool full = w < nw && __ldcg(abits + w) == ~0ull;
+          const unsigned m = __ballot_sync(FULLMASK, !full);
+          if (m) {
+            aw0 += __ffs(m) - 1;
+            break;
+          }
+          aw0 += 32;
+        }
       }
     }
 BFSIM_UNROLL_W
@@ -1024,9 +1310,11 @@ BFSIM_UNROLL_W
   // TPOT terms are buffered (x, k) and evaluated off the critical path.
   auto retire = [&]() {
     const uint32_t kf = static_cast<uint32_t>(k);
-    const uint32_t kh = (GREEDY && H > 0) ? static_cast<uint32_t>(k + H) : kf;
+    constexpr bool kWinPolicy = GREEDY && !NOISY;  // perfect/truncated finish window
+    const bool win = kWinPolicy && H > 0;
+    const uint32_t kh = win ? static_cast<uint32_t>(k + H) : kf;
     const int rk = static_cast<int>(k % Hm);
-    if (GREEDY && H > 0) {
+    if (win) {
 BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         int g = lane + 32 * j;
@@ -1068,7 +1356,7 @@ BFSIM_UNROLL_W
       const uint4 v0 = f4[q], v1 = f4[q + 32], v2 = f4[q + 64], v3 = f4[q + 96];
       const uint32_t m0 = match(v0, kf), m1 = match(v1, kf), m2 = match(v2, kf), m3 = match(v3, kf);
       uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-      if (GREEDY && H > 0) {
+      if (win) {
         e0 = match(v0, kh);
         e1 = match(v1, kh);
         e2 = match(v2, kh);
@@ -1083,7 +1371,7 @@ BFSIM_UNROLL_W
     }
     for (; q < nslot4; q += 32) {
       const uint4 v = f4[q];
-      hit(q, match(v, kf), (GREEDY && H > 0) ? match(v, kh) : 0u);
+      hit(q, match(v, kf), win ? match(v, kh) : 0u);
     }
     __syncwarp();
     int nd = 0;
@@ -1105,6 +1393,13 @@ BFSIM_UNROLL_W
         s_f[slot] = kEmpty;
         cbuf[cb0 + e] = make_int2(s_x[slot], static_cast<int>(k));
         if (emit_reqs) P.reqs.finish_clock[ro + s_id[slot]] = clock;
+      }
+      if constexpr (NOISY) {  // erase_if keeps insertion order (engine.hpp:118-120)
+        int w = 0;
+        for (int p = 0; p < n[j]; ++p) {
+          const uint16_t i = s_lst[p * G + g];
+          if (s_f[g * B + i] != kEmpty) s_lst[(w++) * G + g] = i;
+        }
       }
       n[j] -= nr;
       nd += nr;
@@ -1153,6 +1448,8 @@ BFSIM_UNROLL_W
         int g = lane + 32 * j;
         if (g < G) s_cap[g] = B - n[j];
       }
+    } else if constexpr (NOISY) {
+      gen_normals(act + n_wait, false);  // views are drawn every step (engine.hpp:131)
     }
     // loads, straggler max, dt, clock (engine.hpp:136-146)
     uint32_t lmax = 0;
@@ -1182,7 +1479,7 @@ BFSIM_UNROLL_W
     } else if (s_misc[0] > cbuf_cap - G * B) {
       drain_tpot();  // completion buffer nearly full: evaluate now (ring[k] is written)
     }
-    if (act > 0 || (GREEDY && H > 0)) retire();
+    if (act > 0 || (GREEDY && !NOISY && H > 0)) retire();
     ++k;
     prefetch_fifo();
   }
@@ -1203,6 +1500,7 @@ BFSIM_UNROLL_W
     }
 
   if (emit_steps && k > scap) flags |= BFSIM_FLAG_STEP_OVERFLOW;
+  if (NOISY && __any_sync(FULLMASK, ntie)) flags |= BFSIM_FLAG_NOISE_NEAR_TIE;
   if (lane == 0) {
     bfsim_result_t r;
     r.status = status;
@@ -1237,7 +1535,7 @@ BFSIM_UNROLL_W
   __syncwarp();
 }
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) step_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -1250,13 +1548,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) step_kernel(KParams P) {
     if (lane == 0) qi = atomicAdd(P.queue, 1);
     qi = __shfl_sync(FULLMASK, qi, 0);
     if (qi >= P.n) break;
-    run_traj<MODE, POL, WPL, SMALLC, SM>(P, P.order[qi], sm, ws);
+    run_traj<MODE, POL, WPL, SMALLC, SM, NOISY>(P, P.order[qi], sm, ws);
   }
 }
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY>
 int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
-  auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM>;
+  auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM, NOISY>;
   size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * wpc;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -1269,41 +1567,46 @@ int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
   return static_cast<int>(cudaGetLastError());
 }
 
-template <int MODE, int POL, bool SMALLC, bool SM>
+template <int MODE, int POL, bool SMALLC, bool SM, bool NOISY>
 int launch_w(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
   switch (wpl) {
-    case 1: return launch_t<MODE, POL, 1, SMALLC, SM>(kp, grid, wpc, s, occ);
-    case 2: return launch_t<MODE, POL, 2, SMALLC, SM>(kp, grid, wpc, s, occ);
-    case 4: return launch_t<MODE, POL, 4, SMALLC, SM>(kp, grid, wpc, s, occ);
-    case 8: return launch_t<MODE, POL, 8, SMALLC, SM>(kp, grid, wpc, s, occ);
-    case 16: return launch_t<MODE, POL, 16, SMALLC, SM>(kp, grid, wpc, s, occ);
-    case 32: return launch_t<MODE, POL, 32, SMALLC, SM>(kp, grid, wpc, s, occ);
+    case 1: return launch_t<MODE, POL, 1, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
+    case 2: return launch_t<MODE, POL, 2, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
+    case 4: return launch_t<MODE, POL, 4, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
+    case 8: return launch_t<MODE, POL, 8, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
+    case 16: return launch_t<MODE, POL, 16, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
+    case 32: return launch_t<MODE, POL, 32, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
   }
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
-// Only bfio-greedy uses the class bitmaps, so the FIFO families ignore `small`.
-template <int MODE, int POL>
-int launch_family(int wpl, int small, int all_smem, const KParams& kp, int grid, int wpc,
-                  cudaStream_t s, int* occ) {
-  constexpr bool kClasses = POL == BFSIM_POLICY_BFIO_GREEDY;
-  if (kClasses && !small)
-    return all_smem ? launch_w<MODE, POL, false, true>(wpl, kp, grid, wpc, s, occ)
-                    : launch_w<MODE, POL, false, false>(wpl, kp, grid, wpc, s, occ);
-  return all_smem ? launch_w<MODE, POL, true, true>(wpl, kp, grid, wpc, s, occ)
-                  : launch_w<MODE, POL, true, false>(wpl, kp, grid, wpc, s, occ);
+// One instantiation unit per (mode, policy, class-set kind, noisy): both
+// arena placements (all-shared / spilled) and every workers-per-lane width.
+template <int MODE, int POL, bool SMALLC, bool NOISY>
+int launch_unit(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
+  return kp.plan.all_smem ? launch_w<MODE, POL, SMALLC, true, NOISY>(wpl, kp, grid, wpc, s, occ)
+                          : launch_w<MODE, POL, SMALLC, false, NOISY>(wpl, kp, grid, wpc, s, occ);
 }
 
 }  // namespace detail
 
-#define BFSIM_DECLARE_FAMILY(M, P)                                                            \
-  int launch_family_##M##_##P(int wpl, int small, int all_smem, const KParams& kp, int grid,  \
-                              int wpc, cudaStream_t s, int* occ);
-BFSIM_DECLARE_FAMILY(0, 0)
-BFSIM_DECLARE_FAMILY(0, 1)
-BFSIM_DECLARE_FAMILY(0, 3)
-BFSIM_DECLARE_FAMILY(1, 0)
-BFSIM_DECLARE_FAMILY(1, 1)
-BFSIM_DECLARE_FAMILY(1, 3)
+// Declarations of the instantiation units (engine_<mode>_<policy>*.cu).
+// Only bfio-greedy uses the class bitmaps, so the FIFO units take SMALLC = true.
+#define BFSIM_DECLARE_UNIT(NAME) \
+  int NAME(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ);
+#define BFSIM_DEFINE_UNIT(NAME, M, P, SMALLC, NOISY)                                     \
+  int NAME(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {     \
+    return detail::launch_unit<M, P, SMALLC, NOISY>(wpl, kp, grid, wpc, s, occ);          \
+  }
+BFSIM_DECLARE_UNIT(launch_poisson_fcfs)
+BFSIM_DECLARE_UNIT(launch_poisson_jsq)
+BFSIM_DECLARE_UNIT(launch_poisson_greedy_small)
+BFSIM_DECLARE_UNIT(launch_poisson_greedy_large)
+BFSIM_DECLARE_UNIT(launch_poisson_greedy_noisy_small)
+BFSIM_DECLARE_UNIT(launch_poisson_greedy_noisy_large)
+BFSIM_DECLARE_UNIT(launch_overloaded_fcfs)
+BFSIM_DECLARE_UNIT(launch_overloaded_jsq)
+BFSIM_DECLARE_UNIT(launch_overloaded_greedy_small)
+BFSIM_DECLARE_UNIT(launch_overloaded_greedy_large)
 
 }  // namespace bfsim

@@ -1,9 +1,8 @@
-// Step-kernel instantiations for mode 1 (overloaded), policy 0.
+// Step-kernel instantiation unit: launch_overloaded_fcfs (mode 1, policy 0,
+// small class set = true, noisy lookahead = false). One unit per variant so nvcc
+// compiles them in parallel.
 #include "engine_impl.cuh"
 
 namespace bfsim {
-int launch_family_1_0(int wpl, int small, int all_smem, const KParams& kp, int grid, int wpc,
-                          cudaStream_t s, int* occ) {
-  return detail::launch_family<1, 0>(wpl, small, all_smem, kp, grid, wpc, s, occ);
-}
+BFSIM_DEFINE_UNIT(launch_overloaded_fcfs, 1, 0, true, false)
 }  // namespace bfsim

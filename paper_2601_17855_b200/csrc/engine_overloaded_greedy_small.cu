@@ -1,8 +1,8 @@
-// Step-kernel instantiation unit: launch_overloaded_jsq (mode 1, policy 1,
+// Step-kernel instantiation unit: launch_overloaded_greedy_small (mode 1, policy 3,
 // small class set = true, noisy lookahead = false). One unit per variant so nvcc
 // compiles them in parallel.
 #include "engine_impl.cuh"
 
 namespace bfsim {
-BFSIM_DEFINE_UNIT(launch_overloaded_jsq, 1, 1, true, false)
+BFSIM_DEFINE_UNIT(launch_overloaded_greedy_small, 1, 3, true, false)
 }  // namespace bfsim

@@ -1,9 +1,8 @@
-// Step-kernel instantiations for mode 0 (Poisson), policy 0.
+// Step-kernel instantiation unit: launch_poisson_fcfs (mode 0, policy 0,
+// small class set = true, noisy lookahead = false). One unit per variant so nvcc
+// compiles them in parallel.
 #include "engine_impl.cuh"
 
 namespace bfsim {
-int launch_family_0_0(int wpl, int small, int all_smem, const KParams& kp, int grid, int wpc,
-                          cudaStream_t s, int* occ) {
-  return detail::launch_family<0, 0>(wpl, small, all_smem, kp, grid, wpc, s, occ);
-}
+BFSIM_DEFINE_UNIT(launch_poisson_fcfs, 0, 0, true, false)
 }  // namespace bfsim

@@ -1,9 +1,8 @@
-// Step-kernel instantiations for mode 0 (Poisson), policy 1.
+// Step-kernel instantiation unit: launch_poisson_jsq (mode 0, policy 1,
+// small class set = true, noisy lookahead = false). One unit per variant so nvcc
+// compiles them in parallel.
 #include "engine_impl.cuh"
 
 namespace bfsim {
-int launch_family_0_1(int wpl, int small, int all_smem, const KParams& kp, int grid, int wpc,
-                          cudaStream_t s, int* occ) {
-  return detail::launch_family<0, 1>(wpl, small, all_smem, kp, grid, wpc, s, occ);
-}
+BFSIM_DEFINE_UNIT(launch_poisson_jsq, 0, 1, true, false)
 }  // namespace bfsim

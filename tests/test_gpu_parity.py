@@ -232,3 +232,54 @@ def test_large_worker_counts(ctx, orc):
                        emit_requests=True)
     for i in range(2):
         _ovl_check(orc, br, i, br.scen[i], stream, 64)
+
+
+def test_poisson_noisy_random_batch(ctx, orc):
+    """Noisy lookahead (make_preview policies.hpp:67-90; per-simulation
+    mt19937_64 draws in the order of engine.hpp:131/204-231) on the device:
+    bit-exact against the oracle, which is pinned to the reference build in
+    tests/test_oracle_vs_ref.py. Includes the variants where the draws are
+    unobservable (fcfs/jsq, H = 0, sigma = 0)."""
+    rng = np.random.default_rng(2026)
+    scs, trs = [], []
+    for t in range(80):
+        G = int(rng.integers(1, 70))
+        B = int(rng.integers(1, 20))
+        H = int(rng.choice([1, 2, 3, 8, 20, 20]))
+        pol = abi.BFIO_GREEDY
+        if t % 10 == 9:
+            pol = int(rng.choice([abi.FCFS, abi.JSQ]))
+        if t % 10 == 8:
+            H = 0
+        sigma = float(rng.choice([0.0, 0.5, 2.0, 2.0, 5.0, 40.0])) if t % 10 != 7 else 0.0
+        drift = float(rng.choice([0.0, 1.0, 1.0, 2.0]))
+        rate = float(rng.uniform(3, 25)) * G * B / 8.0
+        s_max = int(rng.choice([2, 7, 64, 100, 700]))
+        tr = host.sample_instance(int(rng.integers(1, 1 << 30)), rate=rate, duration=float(rng.uniform(0.3, 2.0)),
+                                  s_max=s_max, p=float(rng.uniform(0.03, 0.4)))
+        scs.append(abi.scenario(policy=pol, workers=G, batch=B, horizon=H, drift=drift, lookahead=abi.NOISY,
+                                noise_sigma=sigma, seed=int(rng.integers(0, 1 << 62))))
+        trs.append(tr)
+    br = _poisson_batch(ctx, scs, trs)
+    for i, (s, t) in enumerate(zip(br.scen, trs)):
+        assert not int(br.res[i]["flags"]) & abi.FLAG_NOISE_NEAR_TIE
+        check_poisson(orc, br, i, s, t)
+
+
+def test_poisson_c3_slice(ctx, orc, ref):
+    """BASELINE C3 shape (G=64, B=64, lambda=8000/s, bfio-greedy H=20 with
+    Noisy sigma=2), on a 1.5 s prefix of the trace, 3 seeds; seed 1 also
+    against the reference build."""
+    scs, trs = [], []
+    for seed in (1, 2, 3):
+        tr = host.sample_instance(seed, rate=8000.0, duration=1.5, s_max=64, p=0.02)
+        scs.append(abi.scenario(policy=abi.BFIO_GREEDY, workers=64, batch=64, horizon=20,
+                                lookahead=abi.NOISY, noise_sigma=2.0, seed=seed))
+        trs.append(tr)
+    br = _poisson_batch(ctx, scs, trs)
+    for i, (s, t) in enumerate(zip(br.scen, trs)):
+        check_poisson(orc, br, i, s, t)
+    rc, err, (st, rq, m, done) = ref.run_poisson(br.scen[0], trs[0])
+    np.testing.assert_array_equal(br.steps(0)["loads"], st.loads)
+    for k in EXACT:
+        assert float(br.res[0][k]) == m[k]
