@@ -42,7 +42,7 @@ struct DevBuf {
   }
 };
 
-constexpr int kMaxGroups = 16;
+constexpr int kMaxGroups = 16;  // side streams; kernel groups beyond this share them round-robin
 
 }  // namespace
 
@@ -142,6 +142,26 @@ int noisy_variant(const bfsim_scenario_t& s) {
              : 0;
 }
 
+int bits_for(int64_t x) {  // bits to hold values 0..x (the kernel's bits_for)
+  int b = 0;
+  while (b < 63 && (x >> b) > 0) ++b;
+  return b;
+}
+
+// Width of the register-resident lookahead chain (engine_impl.cuh, HR):
+// bfio-greedy with 0 < H < 32 on G <= 64 workers whose per-worker loads fit
+// 31 bits with the worker index and whose horizon costs fit 31 bits.
+int reg_chain_width(const bfsim_scenario_t& s, const bfsim_input_t& in) {
+  if (s.policy != BFSIM_POLICY_BFIO_GREEDY || s.horizon <= 0 || s.horizon >= 32 || s.workers > 64)
+    return 0;
+  const int64_t d = static_cast<int64_t>(s.drift);
+  const int64_t lbound = static_cast<int64_t>(s.batch) * (in.s_max + d * (in.max_decode - 1));
+  const int gbits = std::max(1, bits_for(s.workers - 1));
+  if (bits_for(lbound) + gbits > 31) return 0;
+  if ((static_cast<int64_t>(s.horizon) + 1) * lbound >= (int64_t{1} << 31)) return 0;
+  return s.horizon < 8 ? 8 : 32;
+}
+
 int wpl_for(int G) {
   int w = (G + 31) / 32;
   int p = 1;
@@ -150,7 +170,7 @@ int wpl_for(int G) {
 }
 
 struct Group {
-  int mode, policy, wpl, small, noisy;
+  int mode, policy, wpl, small, noisy, hr;
   std::vector<int32_t> idx;
   Plan plan;
   int wpc = 4, grid = 0;
@@ -363,24 +383,24 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
       return fail(err, errlen, BFSIM_EINVAL, "overloaded scenario without sample streams");
   }
   // group by kernel variant; LPT order inside a group
-  std::map<std::tuple<int, int, int, int, int>, Group> groups;
+  std::map<std::tuple<int, int, int, int, int, int>, Group> groups;
   for (int64_t i = 0; i < n_scen; ++i) {
     const auto& s = scen_host[i];
     const auto& in = inputs_host[s.input_id];
     int small = in.s_max <= 64 ? 1 : 0;
     int wpl = wpl_for(s.workers);
     int noisy = noisy_variant(s);
-    auto key = std::make_tuple(s.mode, s.policy, wpl, small, noisy);
+    int hr = reg_chain_width(s, in);
+    auto key = std::make_tuple(s.mode, s.policy, wpl, small, noisy, hr);
     auto& g = groups[key];
     g.mode = s.mode;
     g.policy = s.policy;
     g.wpl = wpl;
     g.small = small;
     g.noisy = noisy;
+    g.hr = hr;
     g.idx.push_back(static_cast<int32_t>(i));
   }
-  if (static_cast<int>(groups.size()) > kMaxGroups)
-    return fail(err, errlen, BFSIM_EINVAL, "too many distinct kernel variants in one batch");
   std::vector<int32_t> order;
   std::vector<Group*> gl;
   int64_t ws_total = 0;
@@ -406,7 +426,7 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     KParams probe{};
     probe.plan = g.plan;
     int occ = 0;
-    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, g.noisy, probe, 0, g.wpc,
+    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, g.noisy, g.hr, probe, 0, g.wpc,
                                        nullptr, &occ);
     if (rc != 0 || occ <= 0)
       return fail(err, errlen, BFSIM_ECUDA, "step kernel does not fit on the device");
@@ -419,7 +439,8 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
   for (auto* g : gl) order.insert(order.end(), g->idx.begin(), g->idx.end());
   cudaError_t e;
   if ((e = ctx->order.ensure(order.size() * 4)) != cudaSuccess) return cuda_fail(err, errlen, e, "alloc");
-  if ((e = ctx->queue.ensure(kMaxGroups * 4)) != cudaSuccess) return cuda_fail(err, errlen, e, "alloc");
+  if ((e = ctx->queue.ensure(std::max<size_t>(gl.size(), 1) * 4)) != cudaSuccess)
+    return cuda_fail(err, errlen, e, "alloc");
   if ((e = ctx->ws.ensure(static_cast<size_t>(std::max<int64_t>(ws_total, 256)))) != cudaSuccess)
     return cuda_fail(err, errlen, e, "workspace alloc");
   // device copy of the scenario table (the host table is authoritative)
@@ -430,14 +451,14 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
   cudaMemcpyAsync(ctx->scen.p, scen_host, n_scen * sizeof(bfsim_scenario_t), cudaMemcpyHostToDevice, us);
   cudaMemcpyAsync(ctx->inputs.p, inputs_host, n_inputs * sizeof(bfsim_input_t), cudaMemcpyHostToDevice, us);
   cudaMemcpyAsync(ctx->order.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice, us);
-  cudaMemsetAsync(ctx->queue.p, 0, kMaxGroups * 4, us);
+  cudaMemsetAsync(ctx->queue.p, 0, std::max<size_t>(gl.size(), 1) * 4, us);
   int64_t launches = 0;  // counted below: kernels only (not copies / memsets)
   cudaEventRecord(ctx->t0, us);
   cudaEventRecord(ctx->fork, us);
   int64_t off = 0, ws_off = 0;
   for (size_t gi = 0; gi < gl.size(); ++gi) {
     Group& g = *gl[gi];
-    cudaStream_t s = gl.size() == 1 ? us : ctx->side[gi];
+    cudaStream_t s = gl.size() == 1 ? us : ctx->side[gi % kMaxGroups];
     if (gl.size() > 1) cudaStreamWaitEvent(s, ctx->fork, 0);
     KParams kp{};
     kp.scen = static_cast<const bfsim_scenario_t*>(ctx->scen.p);
@@ -453,13 +474,13 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     kp.ws = static_cast<unsigned char*>(ctx->ws.p) + ws_off;
     kp.queue = static_cast<int32_t*>(ctx->queue.p) + gi;
     kp.plan = g.plan;
-    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, g.noisy, kp, g.grid, g.wpc,
+    int rc = bfsim::launch_step_kernel(g.mode, g.policy, g.wpl, g.small, g.noisy, g.hr, kp, g.grid, g.wpc,
                                        s, nullptr);
     if (rc != 0) return cuda_fail(err, errlen, static_cast<cudaError_t>(rc), "step kernel launch");
     ++launches;
     if (gl.size() > 1) {
-      cudaEventRecord(ctx->join[gi], s);
-      cudaStreamWaitEvent(us, ctx->join[gi], 0);
+      cudaEventRecord(ctx->join[gi % kMaxGroups], s);
+      cudaStreamWaitEvent(us, ctx->join[gi % kMaxGroups], 0);
     }
     off += static_cast<int64_t>(g.idx.size());
     ws_off += g.plan.ws_stride * g.grid * g.wpc;

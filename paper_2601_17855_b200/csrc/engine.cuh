@@ -60,7 +60,7 @@ struct KParams {
 
 // Launch one group (grid CTAs of wpc warps) or, when occupancy != NULL, only
 // query CTAs per SM. Returns cudaError_t as int.
-int launch_step_kernel(int mode, int policy, int wpl, int small_classes, int noisy,
+int launch_step_kernel(int mode, int policy, int wpl, int small_classes, int noisy, int hr,
                        const KParams& kp, int grid, int wpc, void* stream, int* occupancy);
 
 }  // namespace bfsim

@@ -293,11 +293,12 @@ struct ClassSet<false> {
 
 // ---------------------------------------------------------------------------
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
 __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned char* ws) {
   constexpr bool OVL = MODE == BFSIM_MODE_OVERLOADED;
   constexpr bool GREEDY = POL == BFSIM_POLICY_BFIO_GREEDY;
   static_assert(!NOISY || (GREEDY && !OVL), "noisy lookahead: Poisson bfio-greedy only");
+  static_assert(HR == 0 || (GREEDY && WPL <= 2), "register lookahead chain: bfio-greedy, G <= 64");
   constexpr bool JSQ = POL == BFSIM_POLICY_JSQ;
   const Plan& pl = P.plan;
   const int lane = threadIdx.x & 31;
@@ -1156,7 +1157,32 @@ BFSIM_UNROLL_W
       }
     } else {
       // general H: lookahead views F_h[g] from the finish window
-      if constexpr (!NOISY) {
+      // (HR > 0: held in registers Fr[j][h], h < HR, for the chain below)
+      int32_t Fr[WPL][HR > 0 ? HR : 1];
+      if constexpr (!NOISY && HR > 0) {
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          const int g = lane + 32 * j;
+          long long PA = 0, PC = 0, Q = 0;
+          int r = static_cast<int>(k % Hm);  // ring row of step k + h - 1
+#pragma unroll
+          for (int h = 0; h < (HR > 0 ? HR : 1); ++h) {
+            long long F = 0;
+            if (h <= H && g < G) {
+              if (h > 0) {
+                PA += s_Wa[r * G + g];
+                PC += s_Wc[r * G + g];
+                Q += PC;
+                r = r + 1 == Hm ? 0 : r + 1;
+              }
+              const long long kh = k + h;
+              F = trunc ? A[j] + d * kh * n[j] - d * Q : (A[j] + d * kh * n[j]) - (PA + d * kh * PC);
+            }
+            Fr[j][h] = static_cast<int32_t>(F);
+          }
+        }
+      }
+      if constexpr (!NOISY && HR == 0) {
 BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           int g = lane + 32 * j;
@@ -1194,66 +1220,156 @@ BFSIM_UNROLL_W
         noisy_views();
         for (int q = lane; q < U; q += 32) o_nz[q] = nzb[act + o_nz[q]];
       }
-      for (int h = lane; h <= H; h += 32) {
-        long long m = 0;
-        for (int g = 0; g < G; ++g) m = s_F[h * G + g] > m ? s_F[h * G + g] : m;
-        s_M[h] = m;
-      }
-      __syncwarp();
-      for (int q = 0; q < U; ++q) {
-        const int c = o_c[q], o = o_o[q];
-        // preview (make_preview, policies.hpp:67-90): w_h = c + d*min(h, o-1)
-        // for h < lim, else 0; lim = predicted completion (perfect: o;
-        // truncated: max(o, H+1); noisy: max(1, o + lround(n)))
-        long long lim = o;
+      if constexpr (HR > 0) {
+        // Register-resident chain (H < HR, G <= 64, every cost < 2^31; the
+        // planner checks the bounds). Lane g holds F_h[g] for its workers and
+        // every lane a copy of M_h = max_g F_h[g]. The placement cost of
+        // worker g is sum_h max(M_h, F_h[g] + w_h) = sum_h w_h +
+        // sum_h max(M_h - w_h, F_h[g]); the first sum does not depend on g,
+        // so the argmin and its ties over (cost, F_0[g], g) are unchanged
+        // (policies.hpp:339-367).
         if constexpr (NOISY) {
-          lim = static_cast<long long>(o) + o_nz[q];
-          lim = lim > 1 ? lim : 1;
-        } else {
-          if (trunc && lim < H + 1) lim = H + 1;
-        }
-        // lane-best (cost, F0, g) over owned workers with a free slot
-        uint64_t bc = ~0ull, bk = ~0ull;
-BFSIM_UNROLL_W
-        for (int j = 0; j < WPL; ++j) {
-          int g = lane + 32 * j;
-          if (g >= G || cp[j] <= 0) continue;
-          long long cost = 0;
-          for (int h = 0; h <= H; ++h) {
-            long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
-            long long v = s_F[h * G + g] + w;
-            long long m = s_M[h];
-            cost += v > m ? v : m;
-          }
-          uint64_t k2 = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
-          if (static_cast<uint64_t>(cost) < bc || (static_cast<uint64_t>(cost) == bc && k2 < bk)) {
-            bc = static_cast<uint64_t>(cost);
-            bk = k2;
+#pragma unroll
+          for (int j = 0; j < WPL; ++j) {
+            const int g = lane + 32 * j;
+#pragma unroll
+            for (int h = 0; h < HR; ++h)
+              Fr[j][h] = (g < G && h <= H) ? static_cast<int32_t>(s_F[h * G + g]) : 0;
           }
         }
-        uint64_t cmin = wmin_u64(bc);
-        uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
-        int gs = static_cast<int>(kmin & gmask);
-BFSIM_UNROLL_W
-        for (int j = 0; j < WPL; ++j)
-          if (lane + 32 * j == gs) {
+        int32_t Mr[HR];
+#pragma unroll
+        for (int h = 0; h < HR; ++h) {
+          int32_t v = 0;
+#pragma unroll
+          for (int j = 0; j < WPL; ++j) v = Fr[j][h] > v ? Fr[j][h] : v;
+          Mr[h] = h <= H ? static_cast<int32_t>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(v))) : 0;
+        }
+        const int32_t d32 = static_cast<int32_t>(d);
+        for (int q = 0; q < U; ++q) {
+          const int c = o_c[q], o = o_o[q];
+          long long lim = o;
+          if constexpr (NOISY) {
+            lim = static_cast<long long>(o) + o_nz[q];
+            lim = lim > 1 ? lim : 1;
+          } else {
+            if (trunc && lim < H + 1) lim = H + 1;
+          }
+          const int32_t lim32 = static_cast<int32_t>(lim < HR ? lim : HR);
+          const int32_t sat = d32 * (o - 1);
+          int32_t wv[HR];
+          uint32_t cost[WPL];
+#pragma unroll
+          for (int j = 0; j < WPL; ++j) cost[j] = 0;
+#pragma unroll
+          for (int h = 0; h < HR; ++h) {
+            const int32_t dh = d32 * h;
+            wv[h] = (h <= H && h < lim32) ? c + (dh < sat ? dh : sat) : 0;
+            if (h <= H) {
+              const int32_t T = Mr[h] - wv[h];
+#pragma unroll
+              for (int j = 0; j < WPL; ++j) cost[j] += static_cast<uint32_t>(T > Fr[j][h] ? T : Fr[j][h]);
+            }
+          }
+          uint64_t best = ~0ull;
+#pragma unroll
+          for (int j = 0; j < WPL; ++j) {
+            const int g = lane + 32 * j;
+            const uint64_t key = (static_cast<uint64_t>(cost[j]) << 32) |
+                                 (static_cast<uint64_t>(static_cast<uint32_t>(Fr[j][0])) << gbits) |
+                                 static_cast<uint64_t>(g);
+            if (g < G && cp[j] > 0 && key < best) best = key;
+          }
+          const uint64_t km = wmin_u64(best);
+          const int gs = static_cast<int>(km & gmask);
+          const int own = gs & 31, jj = gs >> 5;
+#pragma unroll
+          for (int h = 0; h < HR; ++h) {
+            if (h <= H) {
+#pragma unroll
+              for (int j = 0; j < WPL; ++j)
+                if (lane == own && j == jj) Fr[j][h] += wv[h];
+              const int32_t nv = __shfl_sync(FULLMASK, (WPL > 1 && jj) ? Fr[WPL - 1][h] : Fr[0][h], own);
+              Mr[h] = nv > Mr[h] ? nv : Mr[h];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < WPL; ++j)
+            if (lane == own && j == jj) {
+              cp[j] -= 1;
+              A[j] += c + ak;
+              s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
+              adm[j] += 1;
+              if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
+                int r = static_cast<int>((k + o - 1) % Hm);
+                s_Wc[r * G + gs] += 1;
+                s_Wa[r * G + gs] += c + ak;
+              }
+            }
+        }
+        __syncwarp();
+      } else {
+        for (int h = lane; h <= H; h += 32) {
+          long long m = 0;
+          for (int g = 0; g < G; ++g) m = s_F[h * G + g] > m ? s_F[h * G + g] : m;
+          s_M[h] = m;
+        }
+        __syncwarp();
+        for (int q = 0; q < U; ++q) {
+          const int c = o_c[q], o = o_o[q];
+          // preview (make_preview, policies.hpp:67-90): w_h = c + d*min(h, o-1)
+          // for h < lim, else 0; lim = predicted completion (perfect: o;
+          // truncated: max(o, H+1); noisy: max(1, o + lround(n)))
+          long long lim = o;
+          if constexpr (NOISY) {
+            lim = static_cast<long long>(o) + o_nz[q];
+            lim = lim > 1 ? lim : 1;
+          } else {
+            if (trunc && lim < H + 1) lim = H + 1;
+          }
+          // lane-best (cost, F0, g) over owned workers with a free slot
+          uint64_t bc = ~0ull, bk = ~0ull;
+  BFSIM_UNROLL_W
+          for (int j = 0; j < WPL; ++j) {
+            int g = lane + 32 * j;
+            if (g >= G || cp[j] <= 0) continue;
+            long long cost = 0;
             for (int h = 0; h <= H; ++h) {
               long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
-              long long v = s_F[h * G + gs] + w;
-              s_F[h * G + gs] = v;
-              if (v > s_M[h]) s_M[h] = v;
+              long long v = s_F[h * G + g] + w;
+              long long m = s_M[h];
+              cost += v > m ? v : m;
             }
-            cp[j] -= 1;
-            A[j] += c + ak;
-            s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
-            adm[j] += 1;
-            if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
-              int r = static_cast<int>((k + o - 1) % Hm);
-              s_Wc[r * G + gs] += 1;
-              s_Wa[r * G + gs] += c + ak;
+            uint64_t k2 = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
+            if (static_cast<uint64_t>(cost) < bc || (static_cast<uint64_t>(cost) == bc && k2 < bk)) {
+              bc = static_cast<uint64_t>(cost);
+              bk = k2;
             }
           }
-        __syncwarp();
+          uint64_t cmin = wmin_u64(bc);
+          uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
+          int gs = static_cast<int>(kmin & gmask);
+  BFSIM_UNROLL_W
+          for (int j = 0; j < WPL; ++j)
+            if (lane + 32 * j == gs) {
+              for (int h = 0; h <= H; ++h) {
+                long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
+                long long v = s_F[h * G + gs] + w;
+                s_F[h * G + gs] = v;
+                if (v > s_M[h]) s_M[h] = v;
+              }
+              cp[j] -= 1;
+              A[j] += c + ak;
+              s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
+              adm[j] += 1;
+              if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
+                int r = static_cast<int>((k + o - 1) % Hm);
+                s_Wc[r * G + gs] += 1;
+                s_Wa[r * G + gs] += c + ak;
+              }
+            }
+          __syncwarp();
+        }
       }
       for (int q = lane; q < U; q += 32) {
         uint32_t r = s_res[q];
@@ -1535,7 +1651,7 @@ BFSIM_UNROLL_W
   __syncwarp();
 }
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) step_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -1548,13 +1664,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) step_kernel(KParams P) {
     if (lane == 0) qi = atomicAdd(P.queue, 1);
     qi = __shfl_sync(FULLMASK, qi, 0);
     if (qi >= P.n) break;
-    run_traj<MODE, POL, WPL, SMALLC, SM, NOISY>(P, P.order[qi], sm, ws);
+    run_traj<MODE, POL, WPL, SMALLC, SM, NOISY, HR>(P, P.order[qi], sm, ws);
   }
 }
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
 int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
-  auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM, NOISY>;
+  auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM, NOISY, HR>;
   size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * wpc;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -1567,15 +1683,24 @@ int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
   return static_cast<int>(cudaGetLastError());
 }
 
+// hr: register lookahead chain width (0 = shared-memory chain); the planner
+// picks hr > 0 only for bfio-greedy with H < hr and G <= 64.
 template <int MODE, int POL, bool SMALLC, bool SM, bool NOISY>
-int launch_w(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
+int launch_w(int wpl, int hr, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
+  if constexpr (POL == BFSIM_POLICY_BFIO_GREEDY) {
+    if (hr == 8 && wpl == 1) return launch_t<MODE, POL, 1, SMALLC, SM, NOISY, 8>(kp, grid, wpc, s, occ);
+    if (hr == 8 && wpl == 2) return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 8>(kp, grid, wpc, s, occ);
+    if (hr == 32 && wpl == 1) return launch_t<MODE, POL, 1, SMALLC, SM, NOISY, 32>(kp, grid, wpc, s, occ);
+    if (hr == 32 && wpl == 2) return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 32>(kp, grid, wpc, s, occ);
+  }
+  if (hr != 0) return static_cast<int>(cudaErrorInvalidValue);
   switch (wpl) {
-    case 1: return launch_t<MODE, POL, 1, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
-    case 2: return launch_t<MODE, POL, 2, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
-    case 4: return launch_t<MODE, POL, 4, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
-    case 8: return launch_t<MODE, POL, 8, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
-    case 16: return launch_t<MODE, POL, 16, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
-    case 32: return launch_t<MODE, POL, 32, SMALLC, SM, NOISY>(kp, grid, wpc, s, occ);
+    case 1: return launch_t<MODE, POL, 1, SMALLC, SM, NOISY, 0>(kp, grid, wpc, s, occ);
+    case 2: return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 0>(kp, grid, wpc, s, occ);
+    case 4: return launch_t<MODE, POL, 4, SMALLC, SM, NOISY, 0>(kp, grid, wpc, s, occ);
+    case 8: return launch_t<MODE, POL, 8, SMALLC, SM, NOISY, 0>(kp, grid, wpc, s, occ);
+    case 16: return launch_t<MODE, POL, 16, SMALLC, SM, NOISY, 0>(kp, grid, wpc, s, occ);
+    case 32: return launch_t<MODE, POL, 32, SMALLC, SM, NOISY, 0>(kp, grid, wpc, s, occ);
   }
   return static_cast<int>(cudaErrorInvalidValue);
 }
@@ -1583,9 +1708,9 @@ int launch_w(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int*
 // One instantiation unit per (mode, policy, class-set kind, noisy): both
 // arena placements (all-shared / spilled) and every workers-per-lane width.
 template <int MODE, int POL, bool SMALLC, bool NOISY>
-int launch_unit(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
-  return kp.plan.all_smem ? launch_w<MODE, POL, SMALLC, true, NOISY>(wpl, kp, grid, wpc, s, occ)
-                          : launch_w<MODE, POL, SMALLC, false, NOISY>(wpl, kp, grid, wpc, s, occ);
+int launch_unit(int wpl, int hr, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
+  return kp.plan.all_smem ? launch_w<MODE, POL, SMALLC, true, NOISY>(wpl, hr, kp, grid, wpc, s, occ)
+                          : launch_w<MODE, POL, SMALLC, false, NOISY>(wpl, hr, kp, grid, wpc, s, occ);
 }
 
 }  // namespace detail
@@ -1593,10 +1718,10 @@ int launch_unit(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, i
 // Declarations of the instantiation units (engine_<mode>_<policy>*.cu).
 // Only bfio-greedy uses the class bitmaps, so the FIFO units take SMALLC = true.
 #define BFSIM_DECLARE_UNIT(NAME) \
-  int NAME(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ);
-#define BFSIM_DEFINE_UNIT(NAME, M, P, SMALLC, NOISY)                                     \
-  int NAME(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {     \
-    return detail::launch_unit<M, P, SMALLC, NOISY>(wpl, kp, grid, wpc, s, occ);          \
+  int NAME(int wpl, int hr, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ);
+#define BFSIM_DEFINE_UNIT(NAME, M, P, SMALLC, NOISY)                                          \
+  int NAME(int wpl, int hr, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {  \
+    return detail::launch_unit<M, P, SMALLC, NOISY>(wpl, hr, kp, grid, wpc, s, occ);          \
   }
 BFSIM_DECLARE_UNIT(launch_poisson_fcfs)
 BFSIM_DECLARE_UNIT(launch_poisson_jsq)
