@@ -149,17 +149,17 @@ int bits_for(int64_t x) {  // bits to hold values 0..x (the kernel's bits_for)
 }
 
 // Width of the register-resident lookahead chain (engine_impl.cuh, HR):
-// bfio-greedy with 0 < H < 32 on G <= 64 workers whose per-worker loads fit
+// bfio-greedy with 0 < H < 24 on G <= 64 workers whose per-worker loads fit
 // 31 bits with the worker index and whose horizon costs fit 31 bits.
 int reg_chain_width(const bfsim_scenario_t& s, const bfsim_input_t& in) {
-  if (s.policy != BFSIM_POLICY_BFIO_GREEDY || s.horizon <= 0 || s.horizon >= 32 || s.workers > 64)
+  if (s.policy != BFSIM_POLICY_BFIO_GREEDY || s.horizon <= 0 || s.horizon >= 24 || s.workers > 64)
     return 0;
   const int64_t d = static_cast<int64_t>(s.drift);
   const int64_t lbound = static_cast<int64_t>(s.batch) * (in.s_max + d * (in.max_decode - 1));
   const int gbits = std::max(1, bits_for(s.workers - 1));
   if (bits_for(lbound) + gbits > 31) return 0;
   if ((static_cast<int64_t>(s.horizon) + 1) * lbound >= (int64_t{1} << 31)) return 0;
-  return s.horizon < 8 ? 8 : 32;
+  return s.horizon < 8 ? 8 : 24;
 }
 
 int wpl_for(int G) {
@@ -229,7 +229,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   }
   items.push_back({&p.o_stage, GB * 8});
   if (greedy && H > 0) {
-    items.push_back({&p.o_M, (H + 1) * 8LL});
+    items.push_back({&p.o_M, std::max<int64_t>((H + 1) * 8LL, 128)});  // also the register chain row
     items.push_back({&p.o_F, (H + 1) * 8LL * G});
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});

@@ -1222,12 +1222,13 @@ BFSIM_UNROLL_W
       }
       if constexpr (HR > 0) {
         // Register-resident chain (H < HR, G <= 64, every cost < 2^31; the
-        // planner checks the bounds). Lane g holds F_h[g] for its workers and
-        // every lane a copy of M_h = max_g F_h[g]. The placement cost of
-        // worker g is sum_h max(M_h, F_h[g] + w_h) = sum_h w_h +
-        // sum_h max(M_h - w_h, F_h[g]); the first sum does not depend on g,
-        // so the argmin and its ties over (cost, F_0[g], g) are unchanged
-        // (policies.hpp:339-367).
+        // planner checks the bounds). Lane g holds F_h[g] for its workers;
+        // lane h holds M_h = max_g F_h[g] and, per item, w_h and
+        // T_h = M_h - w_h. The placement cost of worker g is
+        // sum_h max(M_h, F_h[g] + w_h) = sum_h w_h + sum_h max(T_h, F_h[g]);
+        // the first sum does not depend on g, so the argmin and its ties over
+        // (cost, F_0[g], g) are unchanged (policies.hpp:339-367).
+        // Entries h > H stay 0 and add nothing; the loops are branch-free.
         if constexpr (NOISY) {
 #pragma unroll
           for (int j = 0; j < WPL; ++j) {
@@ -1237,15 +1238,18 @@ BFSIM_UNROLL_W
               Fr[j][h] = (g < G && h <= H) ? static_cast<int32_t>(s_F[h * G + g]) : 0;
           }
         }
-        int32_t Mr[HR];
+        int32_t Ml = 0;  // M_lane
 #pragma unroll
         for (int h = 0; h < HR; ++h) {
           int32_t v = 0;
 #pragma unroll
           for (int j = 0; j < WPL; ++j) v = Fr[j][h] > v ? Fr[j][h] : v;
-          Mr[h] = h <= H ? static_cast<int32_t>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(v))) : 0;
+          const int32_t m = static_cast<int32_t>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(v)));
+          Ml = lane == h ? m : Ml;
         }
+        int32_t* s_row = reinterpret_cast<int32_t*>(s_M);  // the chosen worker's new F_h row
         const int32_t d32 = static_cast<int32_t>(d);
+        const int32_t dl = d32 * lane;
         for (int q = 0; q < U; ++q) {
           const int c = o_c[q], o = o_o[q];
           long long lim = o;
@@ -1255,21 +1259,20 @@ BFSIM_UNROLL_W
           } else {
             if (trunc && lim < H + 1) lim = H + 1;
           }
-          const int32_t lim32 = static_cast<int32_t>(lim < HR ? lim : HR);
+          const int limH = static_cast<int>(lim < H + 1 ? lim : H + 1);
           const int32_t sat = d32 * (o - 1);
+          const int32_t wl = lane < limH ? c + (dl < sat ? dl : sat) : 0;
+          const int32_t Tl = Ml - wl;
           int32_t wv[HR];
           uint32_t cost[WPL];
 #pragma unroll
           for (int j = 0; j < WPL; ++j) cost[j] = 0;
 #pragma unroll
           for (int h = 0; h < HR; ++h) {
-            const int32_t dh = d32 * h;
-            wv[h] = (h <= H && h < lim32) ? c + (dh < sat ? dh : sat) : 0;
-            if (h <= H) {
-              const int32_t T = Mr[h] - wv[h];
+            const int32_t T = __shfl_sync(FULLMASK, Tl, h);
+            wv[h] = __shfl_sync(FULLMASK, wl, h);
 #pragma unroll
-              for (int j = 0; j < WPL; ++j) cost[j] += static_cast<uint32_t>(T > Fr[j][h] ? T : Fr[j][h]);
-            }
+            for (int j = 0; j < WPL; ++j) cost[j] += static_cast<uint32_t>(T > Fr[j][h] ? T : Fr[j][h]);
           }
           uint64_t best = ~0ull;
 #pragma unroll
@@ -1282,30 +1285,29 @@ BFSIM_UNROLL_W
           }
           const uint64_t km = wmin_u64(best);
           const int gs = static_cast<int>(km & gmask);
-          const int own = gs & 31, jj = gs >> 5;
+          if (lane == (gs & 31)) {
 #pragma unroll
-          for (int h = 0; h < HR; ++h) {
-            if (h <= H) {
+            for (int j = 0; j < WPL; ++j)
+              if (j == (gs >> 5)) {
 #pragma unroll
-              for (int j = 0; j < WPL; ++j)
-                if (lane == own && j == jj) Fr[j][h] += wv[h];
-              const int32_t nv = __shfl_sync(FULLMASK, (WPL > 1 && jj) ? Fr[WPL - 1][h] : Fr[0][h], own);
-              Mr[h] = nv > Mr[h] ? nv : Mr[h];
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < WPL; ++j)
-            if (lane == own && j == jj) {
-              cp[j] -= 1;
-              A[j] += c + ak;
-              s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
-              adm[j] += 1;
-              if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
-                int r = static_cast<int>((k + o - 1) % Hm);
-                s_Wc[r * G + gs] += 1;
-                s_Wa[r * G + gs] += c + ak;
+                for (int h = 0; h < HR; ++h) {
+                  Fr[j][h] += wv[h];
+                  s_row[h] = Fr[j][h];
+                }
+                cp[j] -= 1;
+                A[j] += c + ak;
+                s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
+                adm[j] += 1;
+                if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
+                  int r = static_cast<int>((k + o - 1) % Hm);
+                  s_Wc[r * G + gs] += 1;
+                  s_Wa[r * G + gs] += c + ak;
+                }
               }
-            }
+          }
+          __syncwarp();
+          if (lane < HR) Ml = s_row[lane] > Ml ? s_row[lane] : Ml;
+          __syncwarp();
         }
         __syncwarp();
       } else {
@@ -1684,14 +1686,14 @@ int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
 }
 
 // hr: register lookahead chain width (0 = shared-memory chain); the planner
-// picks hr > 0 only for bfio-greedy with H < hr and G <= 64.
+// picks hr in {8, 24} only for bfio-greedy with H < hr and G <= 64.
 template <int MODE, int POL, bool SMALLC, bool SM, bool NOISY>
 int launch_w(int wpl, int hr, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
   if constexpr (POL == BFSIM_POLICY_BFIO_GREEDY) {
     if (hr == 8 && wpl == 1) return launch_t<MODE, POL, 1, SMALLC, SM, NOISY, 8>(kp, grid, wpc, s, occ);
     if (hr == 8 && wpl == 2) return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 8>(kp, grid, wpc, s, occ);
-    if (hr == 32 && wpl == 1) return launch_t<MODE, POL, 1, SMALLC, SM, NOISY, 32>(kp, grid, wpc, s, occ);
-    if (hr == 32 && wpl == 2) return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 32>(kp, grid, wpc, s, occ);
+    if (hr == 24 && wpl == 1) return launch_t<MODE, POL, 1, SMALLC, SM, NOISY, 24>(kp, grid, wpc, s, occ);
+    if (hr == 24 && wpl == 2) return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 24>(kp, grid, wpc, s, occ);
   }
   if (hr != 0) return static_cast<int>(cudaErrorInvalidValue);
   switch (wpl) {
