@@ -32,7 +32,7 @@ def nvcc() -> str:
 
 def _flags():
     return [
-        "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+        "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xfatbin=-compress-all", "-Xcompiler", "-fPIC",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-diag-suppress", "177",
     ]
 

@@ -240,6 +240,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_lst, GB * 2});
     items.push_back({&p.o_onz, GB * 4});
   }
+  if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8});
   if (greedy) {
     items.push_back({&p.o_res, GB * 4});
     items.push_back({&p.o_pcl, GB * 4});

@@ -39,6 +39,8 @@ struct Plan {
   // noisy lookahead: mt19937_64 state, per-worker active lists, per-item
   // draws (hot); the step's draws, admitted-id bitmap and its word prefix (cold)
   int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre;
+  // bfio-greedy with WPL >= 16: per-worker argmin keys
+  int64_t o_key;
   int cbuf, noisy;
 };
 

@@ -131,22 +131,27 @@ __device__ __forceinline__ void mt_seed(uint64_t* mt, uint64_t seed) {
 // fenced from its writes by __syncwarp).
 __device__ __forceinline__ void mt_twist(uint64_t* mt) {
   const int lane = threadIdx.x & 31;
-  for (int b = 0; b < kMtM; b += 32) {
-    const int i = b + lane;
-    uint64_t v = 0;
-    if (i < kMtM) v = mt_mix(mt[i], mt[i + 1], mt[i + kMtM]);
-    __syncwarp();
-    if (i < kMtM) mt[i] = v;
-    __syncwarp();
+  uint64_t v[5];
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {  // i < 156: all reads before any write
+    const int i = lane + 32 * t;
+    v[t] = i < kMtM ? mt_mix(mt[i], mt[i + 1], mt[i + kMtM]) : 0ull;
   }
-  for (int b = kMtM; b < kMtN; b += 32) {
-    const int i = b + lane;
-    uint64_t v = 0;
-    if (i < kMtN) v = mt_mix(mt[i], mt[i + 1 < kMtN ? i + 1 : 0], mt[i - kMtM]);
-    __syncwarp();
-    if (i < kMtN) mt[i] = v;
-    __syncwarp();
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 5; ++t)
+    if (lane + 32 * t < kMtM) mt[lane + 32 * t] = v[t];
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {  // 156 <= i < 312
+    const int i = kMtM + lane + 32 * t;
+    v[t] = i < kMtN ? mt_mix(mt[i], mt[i + 1 < kMtN ? i + 1 : 0], mt[i - kMtM]) : 0ull;
   }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < 5; ++t)
+    if (kMtM + lane + 32 * t < kMtN) mt[kMtM + lane + 32 * t] = v[t];
+  __syncwarp();
 }
 
 // generate_canonical<double, 53>: (double)u / 2^64, clamped below 1.
@@ -367,6 +372,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* s_misc = at<SM, int32_t>(sm, ws, pl.o_misc);  // [0] completion-buffer fill
   int32_t* o_o = at<SM, int32_t>(sm, ws, pl.o_oo);
   int32_t* o_id = at<SM, int32_t>(sm, ws, pl.o_oid);
+  uint64_t* s_key = (GREEDY && WPL >= 16) ? at<SM, uint64_t>(sm, ws, pl.o_key) : nullptr;
   // Noisy lookahead (NOISY): engine state, per-worker active lists in
   // insertion order (interleaved [pos * G + g]), per-item draws, the step's
   // draws and the admitted-id bitmap that gives waiting ranks.
@@ -703,40 +709,57 @@ BFSIM_UNROLL_W
         mt_twist(s_mt);
         mt_i = 0;
       }
-      const int pi = mt_i + 2 * lane;
-      const bool valid = pi < kMtN;
-      double y = 0.0, r2 = 0.0;
-      bool acc = false;
-      if (valid) {
+      // every remaining pair of the block at once: pair mt_i/2 + 32t + lane
+      const int np = (kMtN - mt_i) >> 1;
+      double yv[5], r2v[5];
+      unsigned am[5];
+      int before[5];
+      int run = 0;
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const int pq = 32 * t + lane;
+        const bool valid = pq < np;
+        const int pi = mt_i + 2 * (valid ? pq : 0);
         const double u1 = mt_canonical(mt_temper(s_mt[pi]));
         const double u2 = mt_canonical(mt_temper(s_mt[pi + 1]));
         const double x = __dsub_rn(__dmul_rn(2.0, u1), 1.0);
-        y = __dsub_rn(__dmul_rn(2.0, u2), 1.0);
-        r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
-        acc = !(r2 > 1.0 || r2 == 0.0);
+        yv[t] = __dsub_rn(__dmul_rn(2.0, u2), 1.0);
+        r2v[t] = __dadd_rn(__dmul_rn(x, x), __dmul_rn(yv[t], yv[t]));
+        am[t] = __ballot_sync(FULLMASK, valid && !(r2v[t] > 1.0 || r2v[t] == 0.0));
+        before[t] = run;
+        run += __popc(am[t]);
       }
-      const unsigned am = __ballot_sync(FULLMASK, acc);
-      const unsigned vm = __ballot_sync(FULLMASK, valid);
+      if (values) {
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          const long long r = got + before[t] + __popc(am[t] & lanemask_lt());
+          const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2v[t])), r2v[t]));
+          const double nv = __dadd_rn(__dmul_rn(__dmul_rn(yv[t], mult), sigma), 0.0);
+          if (((am[t] >> lane) & 1u) && r < D) {
+            long long lr = llround(nv);
+            lr = lr > (1ll << 30) ? (1ll << 30) : (lr < -(1ll << 30) ? -(1ll << 30) : lr);
+            nzb[r] = static_cast<int32_t>(lr);
+            // CUDA log is within 1 ulp of glibc's; only a draw this close to
+            // a half-integer could round differently
+            const double av = fabs(nv);
+            if (fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
+          }
+        }
+      }
       const long long need = D - got;
-      const long long r = got + __popc(am & lanemask_lt());
-      if (values && acc && r < D) {
-        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
-        const double nv = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), sigma), 0.0);
-        long long lr = llround(nv);
-        lr = lr > (1ll << 30) ? (1ll << 30) : (lr < -(1ll << 30) ? -(1ll << 30) : lr);
-        nzb[r] = static_cast<int32_t>(lr);
-        // CUDA log is within 1 ulp of glibc's; only a draw this close to a
-        // half-integer could round differently
-        const double av = fabs(nv);
-        if (fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
-      }
-      const int nacc = __popc(am);
-      if (nacc >= need) {
-        mt_i += 2 * (static_cast<int>(__fns(am, 0, static_cast<int>(need))) + 1);
+      if (run >= need) {
+        int rest = static_cast<int>(need), used = 0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          const int c = __popc(am[t]);
+          if (rest > 0 && rest <= c) used = 32 * t + static_cast<int>(__fns(am[t], 0, rest)) + 1;
+          rest -= c;
+        }
+        mt_i += 2 * used;
         got = D;
       } else {
-        mt_i += 2 * __popc(vm);
-        got += nacc;
+        mt_i = kMtN;
+        got += run;
       }
     }
     __syncwarp();
@@ -855,6 +878,9 @@ BFSIM_UNROLL_W
       else if (g < G && cap0[j] > 0 && n[j] < vext) vext = n[j];
     }
     int nl = 0, T = 0;
+    // fully served levels end at vfull (-1: none); at most the last level,
+    // vpart, is served partially (its first takep workers in index order)
+    int vfull = -1, vpart = -1, takep = 0;
     if (!JSQ) {
       // Alg. 3: argmax cap, lowest index first. Level v (cap value, descending)
       // serves every worker with cap0 >= v in index order.
@@ -872,6 +898,11 @@ BFSIM_UNROLL_W
           lvT[nl] = T;
           lvV[nl] = v;
           lvK[nl] = take;
+        }
+        if (take == cnt) vfull = v;
+        else {
+          vpart = v;
+          takep = take;
         }
         T += take;
       }
@@ -894,71 +925,79 @@ BFSIM_UNROLL_W
           lvV[nl] = v;
           lvK[nl] = take;
         }
+        if (take == cnt) vfull = v;
+        else {
+          vpart = v;
+          takep = take;
+        }
         T += take;
       }
     }
     if (SM) cp_async_wait_all();
     __syncwarp();
-    // item-parallel placement: admission t takes waiting request head + t
-    for (int t = lane; t < U; t += 32) {
-      int l = 0;
-      while (l + 1 < nl && lvT[l + 1] <= t) ++l;
-      int pos = t - lvT[l];
-      int g = 0;
-BFSIM_UNROLL_W
-      for (int j = 0; j < WPL; ++j) {
-        uint32_t mk = lvM[l * WPL + j];
-        int c = __popc(mk);
-        if (pos >= 0 && pos < c) {
-          g = static_cast<int>(__fns(mk, 0, pos + 1)) + 32 * j;
-          pos = -1;
-        } else if (pos >= 0) {
-          pos -= c;
+    // placement, segment by segment: level l, worker block j holds the
+    // next min(popc, left) admissions in worker-index order; admission t
+    // takes waiting request head + t
+    {
+      int t0 = 0;
+      for (int l = 0; l < nl; ++l) {
+        int left = lvK[l];
+        const int vl = lvV[l];
+        for (int j = 0; j < WPL && left > 0; ++j) {
+          const uint32_t mk = lvM[l * WPL + j];
+          int c = __popc(mk);
+          c = c < left ? c : left;
+          for (int i = lane; i < c; i += 32) {
+            const int g = static_cast<int>(__fns(mk, 0, i + 1)) + 32 * j;
+            const int t = t0 + i;
+            const int rank = JSQ ? vl - (B - s_capb[g]) : s_capb[g] - vl;
+            const long long id = head + t;
+            int s, o;
+            if (SM && t < umax) {
+              int2 v = stage[t];
+              s = v.x;
+              o = v.y;
+            } else if (OVL) {
+              int2 v = __ldg(reinterpret_cast<const int2*>(st) + id);
+              s = v.x;
+              o = v.y;
+            } else {
+              int4 v = __ldg(reinterpret_cast<const int4*>(tr) + id);
+              s = v.z;
+              o = v.w;
+            }
+            if (OVL) atomicAdd(&c_rec[s].x, 1);  // leaves the pool (class count for Def. 1)
+            place(g, rank, id, s, o);
+            atomicAdd(&s_asum[g], static_cast<unsigned long long>(static_cast<long long>(s) - d * k));
+          }
+          t0 += c;
+          left -= c;
         }
       }
-      int rank = JSQ ? lvV[l] - (B - s_capb[g]) : s_capb[g] - lvV[l];
-      long long id = head + t;
-      int s, o;
-      if (SM && t < umax) {
-        int2 v = stage[t];
-        s = v.x;
-        o = v.y;
-      } else if (OVL) {
-        int2 v = __ldg(reinterpret_cast<const int2*>(st) + id);
-        s = v.x;
-        o = v.y;
-      } else {
-        int4 v = __ldg(reinterpret_cast<const int4*>(tr) + id);
-        s = v.z;
-        o = v.w;
-      }
-      if (OVL) atomicAdd(&c_rec[s].x, 1);  // leaves the pool (class count for Def. 1)
-      place(g, rank, id, s, o);
-      atomicAdd(&s_asum[g], static_cast<unsigned long long>(static_cast<long long>(s) - d * k));
     }
     __syncwarp();
+    // admissions per worker in closed form: every fully served level the
+    // worker is eligible for, plus its rank in the partial level
+    {
+      int before = 0;
 BFSIM_UNROLL_W
-    for (int j = 0; j < WPL; ++j) {
-      int g = lane + 32 * j;
-      if (g >= G) continue;
-      int adm = 0;
-      for (int l = 0; l < nl; ++l) {
-        int before = 0;
-        bool mine = false;
-BFSIM_UNROLL_W
-        for (int j2 = 0; j2 < WPL; ++j2) {
-          uint32_t mk = lvM[l * WPL + j2];
-          if (j2 < j) before += __popc(mk);
-          if (j2 == j) {
-            mine = (mk >> lane) & 1u;
-            before += __popc(mk & lanemask_lt());
-          }
+      for (int j = 0; j < WPL; ++j) {
+        const int g = lane + 32 * j;
+        int adm = 0;
+        if (g < G) {
+          if (!JSQ) adm = vfull >= 1 && cap0[j] >= vfull ? cap0[j] - vfull + 1 : 0;
+          else adm = vfull >= 0 && cap0[j] > 0 && n[j] <= vfull ? vfull - n[j] + 1 : 0;
         }
-        if (mine && before < lvK[l]) ++adm;
+        const bool elig = vpart >= 0 && g < G && (JSQ ? n[j] <= vpart : cap0[j] >= vpart);
+        const unsigned mk = __ballot_sync(FULLMASK, elig);
+        if (elig && before + __popc(mk & lanemask_lt()) < takep) ++adm;
+        before += __popc(mk);
+        if (g < G) {
+          n[j] += adm;
+          A[j] += static_cast<long long>(s_asum[g]);
+          s_asum[g] = 0;
+        }
       }
-      n[j] += adm;
-      A[j] += static_cast<long long>(s_asum[g]);
-      s_asum[g] = 0;
     }
     head += U;
     __syncwarp();
@@ -994,6 +1033,33 @@ BFSIM_UNROLL_W
       if constexpr (K32) return __reduce_min_sync(FULLMASK, key);
       else return wmin_u64(key);
     };
+    // WPL >= 16 (G > 256): the lane arrays live in local memory, so a lane
+    // does not rescan its workers after a pick. Worker keys sit in s_key and
+    // the owner lane's best is re-reduced by the whole warp (one load each).
+    constexpr bool kCoop = WPL >= 16;
+    auto coop_init = [&](const long long* ld, const int* fr) {
+      if constexpr (kCoop) {
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j) {
+          const int g = lane + 32 * j;
+          s_key[g] = fr[j] > 0 ? (static_cast<uint64_t>(ld[j]) << gbits) | static_cast<uint64_t>(g)
+                               : ~0ull;
+        }
+        __syncwarp();
+      }
+    };
+    // after worker gs changed: its owner lane's new best, reduced cooperatively
+    auto coop_best = [&](int gs, key_t lk) -> key_t {
+      if constexpr (kCoop) {
+        __syncwarp();
+        const int own = gs & 31;
+        const key_t v = lane < WPL ? static_cast<key_t>(s_key[own + 32 * lane]) : KMAX;
+        const key_t m = wmin(v);
+        return lane == own ? m : lk;
+      } else {
+        return lk;
+      }
+    };
     // prefetch one deque entry into the stage (async; waited before resolution)
     auto fetch = [&](int slot, int base, int idx) {
       if constexpr (SM) cp_async8(&stage[slot], &deq[base + idx]);
@@ -1016,6 +1082,7 @@ BFSIM_UNROLL_W
       long long target = static_cast<long long>(
           __reduce_max_sync(FULLMASK, static_cast<uint32_t>(tmax)));
       key_t lk = lane_key(ld, fr);
+      coop_init(ld, fr);
       for (int q = 0; q < U; ++q) {
         const key_t km = wmin(lk);
         const long long lmin = static_cast<long long>(km >> gbits);
@@ -1038,13 +1105,24 @@ BFSIM_UNROLL_W
           fetch(q, cr.w, idx);
         }
         if constexpr (!SMALLC) pset.add_uniform(c);
-BFSIM_UNROLL_W
-        for (int j = 0; j < WPL; ++j)
-          if (lane + 32 * j == gs) {
-            ld[j] += c;
-            fr[j] -= 1;
+        if constexpr (kCoop) {
+          if (lane == (gs & 31)) {
+            const int jj = gs >> 5;
+            ld[jj] += c;
+            fr[jj] -= 1;
+            s_key[gs] = fr[jj] > 0 ? (static_cast<uint64_t>(ld[jj]) << gbits) | static_cast<uint64_t>(gs)
+                                   : ~0ull;
           }
-        lk = lane_key(ld, fr);
+          lk = coop_best(gs, lk);
+        } else {
+BFSIM_UNROLL_W
+          for (int j = 0; j < WPL; ++j)
+            if (lane + 32 * j == gs) {
+              ld[j] += c;
+              fr[j] -= 1;
+            }
+          lk = lane_key(ld, fr);
+        }
         const long long nl = lmin + c;
         target = nl > target ? nl : target;
       }
@@ -1130,22 +1208,37 @@ BFSIM_UNROLL_W
       // placement (policies.hpp:339-367) at H = 0: argmin (load, index) over
       // workers with a free slot (F3), one warp reduction per item
       key_t lk = lane_key(F0, cp);
+      coop_init(F0, cp);
       int cnext = o_c[0];
       for (int j = 0; j < U; ++j) {
         const int c = cnext;
         if (j + 1 < U) cnext = o_c[j + 1];
         const key_t km = wmin(lk);
         const int gs = static_cast<int>(km) & static_cast<int>(gmask);
-BFSIM_UNROLL_W
-        for (int jj = 0; jj < WPL; ++jj)
-          if (lane + 32 * jj == gs) {
+        if constexpr (kCoop) {
+          if (lane == (gs & 31)) {
+            const int jj = gs >> 5;
             F0[jj] += c;
             cp[jj] -= 1;
             A[jj] += c + ak;
             s_res[j] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[jj]) << 16);
             adm[jj] += 1;
+            s_key[gs] = cp[jj] > 0 ? (static_cast<uint64_t>(F0[jj]) << gbits) | static_cast<uint64_t>(gs)
+                                   : ~0ull;
           }
-        lk = lane_key(F0, cp);
+          lk = coop_best(gs, lk);
+        } else {
+BFSIM_UNROLL_W
+          for (int jj = 0; jj < WPL; ++jj)
+            if (lane + 32 * jj == gs) {
+              F0[jj] += c;
+              cp[jj] -= 1;
+              A[jj] += c + ak;
+              s_res[j] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[jj]) << 16);
+              adm[jj] += 1;
+            }
+          lk = lane_key(F0, cp);
+        }
       }
       if (SM) cp_async_wait_all();
       __syncwarp();
