@@ -194,7 +194,9 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     max_len = std::max<int64_t>(max_len, in.length);
   }
   int R = 1;
-  while (R <= max_o + 33) R <<= 1;  // admit clocks stay readable until the 32-step TPOT drain
+  // admit clocks stay readable until the 32-step TPOT drain; calendar
+  // buckets k .. k + max(max_o, H) never alias
+  while (R <= max_o + 33 + H) R <<= 1;
   p.G = G;
   p.B = B;
   p.H = H;
@@ -276,6 +278,13 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   };
   cold(&p.o_ring, R * 8LL);
   cold(&p.o_cbuf, static_cast<int64_t>(p.cbuf) * 8);
+  // completion calendar instead of the per-step finish-step scan once the
+  // slot arrays outgrow shared memory
+  p.cal = GB > 4096 ? 1 : 0;
+  if (p.cal) {
+    cold(&p.o_calh, static_cast<int64_t>(R) * 32 * 4);
+    cold(&p.o_calnx, GB * 4);
+  }
   if (greedy) cold(&p.o_deq, max_len * 8);
   else p.o_deq = -1;
   if (g.noisy) {

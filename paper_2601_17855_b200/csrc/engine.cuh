@@ -41,6 +41,9 @@ struct Plan {
   int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre;
   // bfio-greedy with WPL >= 16: per-worker argmin keys
   int64_t o_key;
+  // completion calendar (cal != 0, large G*B): list heads [R][32], per-slot links
+  int64_t o_calh, o_calnx;
+  int cal, reserved3;
   int cbuf, noisy;
 };
 

@@ -373,6 +373,11 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* o_o = at<SM, int32_t>(sm, ws, pl.o_oo);
   int32_t* o_id = at<SM, int32_t>(sm, ws, pl.o_oid);
   uint64_t* s_key = (GREEDY && WPL >= 16) ? at<SM, uint64_t>(sm, ws, pl.o_key) : nullptr;
+  // Completion calendar (large G*B): bucket f mod R holds, per owner lane
+  // (g mod 32), a linked list of the slots finishing at step f.
+  const bool cal = pl.cal != 0;
+  int32_t* calh = cal ? gat<int32_t>(ws, pl.o_calh) : nullptr;
+  int32_t* calnx = cal ? gat<int32_t>(ws, pl.o_calnx) : nullptr;
   // Noisy lookahead (NOISY): engine state, per-worker active lists in
   // insertion order (interleaved [pos * G + g]), per-item draws, the step's
   // draws and the admitted-id bitmap that gives waiting ranks.
@@ -410,6 +415,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     wset.init(bm, bm + 64, S);
     pset.init(pbm, pbm + 64, S);
   }
+  if (cal)
+    for (int i = lane; i < pl.R * 32; i += 32) calh[i] = -1;
   int mt_i = kMtN;       // next engine word in the current block (always even)
   long long aw0 = 0;     // first bitmap word holding a waiting (revealed, unadmitted) id
   bool ntie = false;     // a draw landed next to an lround tie (BFSIM_FLAG_NOISE_NEAR_TIE)
@@ -687,6 +694,10 @@ BFSIM_UNROLL_W
     s_a[slot] = static_cast<int32_t>(s - d * k);
     s_x[slot] = static_cast<int32_t>(k);
     s_id[slot] = static_cast<int32_t>(id);
+    if (cal) {
+      const int b = static_cast<int>((k + o - 1) & Rm);
+      calnx[slot] = atomicExch(&calh[b * 32 + (g & 31)], slot);
+    }
     if (emit_reqs) {
       P.reqs.start_step[ro + id] = static_cast<int32_t>(k);
       P.reqs.worker[ro + id] = g;
@@ -1536,6 +1547,83 @@ BFSIM_UNROLL_W
       }
       __syncwarp();
     }
+    auto slot_worker = [&](int slot) -> int {
+      int g = static_cast<int>(static_cast<float>(slot) * invB);
+      g -= (g * B > slot) ? 1 : 0;
+      g += ((g + 1) * B <= slot) ? 1 : 0;
+      return g;
+    };
+    if (cal) {
+      // Calendar: each lane walks its own lists (it owns every worker on
+      // them, so worker state needs no atomics). Window entries first: the
+      // slots finishing at k + H stay listed.
+      if (win) {
+        for (int s = calh[static_cast<int>((k + H) & Rm) * 32 + lane]; s >= 0; s = calnx[s]) {
+          const int g = slot_worker(s);
+          s_Wc[rk * G + g] += 1;
+          s_Wa[rk * G + g] += s_a[s];
+        }
+      }
+      const int b = static_cast<int>(k & Rm);
+      int s = calh[b * 32 + lane];
+      calh[b * 32 + lane] = -1;
+      int rc[WPL];
+BFSIM_UNROLL_W
+      for (int j = 0; j < WPL; ++j) rc[j] = 0;
+      int nd = 0;
+      while (__any_sync(FULLMASK, s >= 0)) {
+        const bool live = s >= 0;
+        const unsigned am = __ballot_sync(FULLMASK, live);
+        const int leader = __ffs(am) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&s_misc[0], __popc(am));
+        base = __shfl_sync(FULLMASK, base, leader);
+        if (live) {
+          const int slot = s;
+          s = calnx[slot];
+          const int g = slot_worker(slot);
+          const int i = slot - g * B;
+          const int jj = g >> 5;
+          const long long av = s_a[slot];
+          if constexpr (WPL > 8) {  // lane arrays in local memory: index directly
+            A[jj] -= av;
+            s_stk[g * B + B - n[jj] + rc[jj]] = static_cast<uint16_t>(i);
+            rc[jj] += 1;
+          } else {
+#pragma unroll
+            for (int j = 0; j < WPL; ++j)
+              if (j == jj) {
+                A[j] -= av;
+                s_stk[g * B + B - n[j] + rc[j]] = static_cast<uint16_t>(i);
+                rc[j] += 1;
+              }
+          }
+          s_f[slot] = kEmpty;
+          cbuf[base + __popc(am & lanemask_lt())] = make_int2(s_x[slot], static_cast<int>(k));
+          if (emit_reqs) P.reqs.finish_clock[ro + s_id[slot]] = clock;
+          ++nd;
+        }
+      }
+      __syncwarp();
+BFSIM_UNROLL_W
+      for (int j = 0; j < WPL; ++j) {
+        const int g = lane + 32 * j;
+        if (g >= G || rc[j] == 0) continue;
+        if constexpr (NOISY) {  // erase_if keeps insertion order (engine.hpp:118-120)
+          int w = 0;
+          for (int p = 0; p < n[j]; ++p) {
+            const uint16_t i = s_lst[p * G + g];
+            if (s_f[g * B + i] != kEmpty) s_lst[(w++) * G + g] = i;
+          }
+        }
+        n[j] -= rc[j];
+        s_cap[g] = B - n[j];
+      }
+      const long long ndw = static_cast<long long>(__reduce_add_sync(FULLMASK, static_cast<unsigned>(nd)));
+      done += ndw;
+      act -= ndw;
+      return;
+    }
     const int nslot4 = (G * B + 3) >> 2;
     const uint4* f4 = reinterpret_cast<const uint4*>(s_f);
     auto match = [&](uint4 v, uint32_t key) -> uint32_t {
@@ -1549,9 +1637,7 @@ BFSIM_UNROLL_W
         m &= ~(1u << c);
         me &= ~(1u << c);
         const int slot = 4 * q + c;
-        int g = static_cast<int>(static_cast<float>(slot) * invB);
-        g -= (g * B > slot) ? 1 : 0;
-        g += ((g + 1) * B <= slot) ? 1 : 0;
+        const int g = slot_worker(slot);
         if (fin) {
           const int pos = atomicAdd(&s_rn[g], 1);
           s_rlist[g * B + pos] = static_cast<uint16_t>(slot - g * B);

@@ -283,3 +283,30 @@ def test_poisson_c3_slice(ctx, orc, ref):
     np.testing.assert_array_equal(br.steps(0)["loads"], st.loads)
     for k in EXACT:
         assert float(br.res[0][k]) == m[k]
+
+
+def test_calendar_large_slot_counts(ctx, orc):
+    """G*B > 4096 switches retirement from the per-step finish-step scan to the
+    completion calendar (per-owner-lane lists per finish step); every policy,
+    the perfect/truncated lookahead window, noisy lists, and run_overloaded."""
+    scs, trs = [], []
+    cases = ((128, 40, abi.FCFS, 0, abi.PERFECT), (100, 50, abi.JSQ, 0, abi.PERFECT),
+             (96, 48, abi.BFIO_GREEDY, 0, abi.PERFECT), (64, 80, abi.BFIO_GREEDY, 6, abi.PERFECT),
+             (70, 64, abi.BFIO_GREEDY, 20, abi.TRUNCATED), (300, 16, abi.BFIO_GREEDY, 3, abi.PERFECT),
+             (64, 72, abi.BFIO_GREEDY, 20, abi.NOISY), (520, 9, abi.BFIO_GREEDY, 0, abi.PERFECT))
+    for t, (G, B, pol, H, la) in enumerate(cases):
+        scs.append(abi.scenario(policy=pol, workers=G, batch=B, horizon=H, lookahead=la,
+                                noise_sigma=2.0 if la == abi.NOISY else 0.0, seed=t + 1))
+        trs.append(host.sample_instance(100 + t, rate=G * B * 1.5, duration=0.8, s_max=64, p=0.05))
+    br = _poisson_batch(ctx, scs, trs)
+    for i, (s, t) in enumerate(zip(br.scen, trs)):
+        check_poisson(orc, br, i, s, t)
+    stream = host.sample_stream(21, 400000, s_max=64, p=0.05)
+    so = [abi.scenario(mode=abi.OVERLOADED, policy=p, workers=1024, batch=8, horizon=H, steps=40, warmup=10,
+                       seed=21) for p, H in ((abi.FCFS, 0), (abi.JSQ, 0), (abi.BFIO_GREEDY, 0), (abi.BFIO_GREEDY, 2))]
+    for s in so:
+        s["input_id"] = 0
+    br = ctx.run_batch(np.array(so, abi.scenario_dtype), host.InputPool([stream]), emit_steps=True,
+                       emit_requests=True)
+    for i in range(len(so)):
+        _ovl_check(orc, br, i, br.scen[i], stream, 64)
