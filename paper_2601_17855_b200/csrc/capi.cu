@@ -215,34 +215,44 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     int64_t* code;
     int64_t bytes;
   };
-  // hot first
+  // completion calendar instead of the per-step finish-step scan once the
+  // slot arrays outgrow shared memory (the scan's per-worker lists go away)
+  p.cal = GB > 4096 ? 1 : 0;
+  p.noisy = g.noisy;
+  p.cbuf = static_cast<int>(std::min<int64_t>(GB + 512, 1 << 24));
+  // Hot and small first (first fit: an array that does not fit spills to
+  // the warp's global workspace and later, smaller ones may still fit):
+  // per-step scalars and per-worker state, class records, argmin keys, the
+  // accounting ring, then the per-slot arrays, then per-admission scratch.
   std::vector<Item> items = {
-      {&p.o_rl, 32LL * rstride * 4}, {&p.o_rdt, 32 * 8}, {&p.o_rcs, 32 * 8}, {&p.o_rmx, 32 * 4},
-      {&p.o_rac, 32 * 4},            {&p.o_capb, G * 4LL}, {&p.o_asum, G * 8LL},
-      {&p.o_cap, G * 4LL},           {&p.o_rn, G * 4LL},  {&p.o_rlist, GB * 2},
-      {&p.o_lvT, lvl * 4},           {&p.o_lvV, lvl * 4}, {&p.o_lvK, lvl * 4},
-      {&p.o_lvM, lvl * wpl * 4},     {&p.o_f, ((GB + 3) & ~3LL) * 4},    {&p.o_stk, GB * 2},
-      {&p.o_a, GB * 4},              {&p.o_x, GB * 4},    {&p.o_id, GB * 4},
+      {&p.o_rdt, 32 * 8}, {&p.o_rcs, 32 * 8}, {&p.o_rmx, 32 * 4}, {&p.o_rac, 32 * 4},
+      {&p.o_misc, 16},    {&p.o_capb, G * 4LL}, {&p.o_asum, G * 8LL}, {&p.o_cap, G * 4LL},
+      {&p.o_rn, G * 4LL}, {&p.o_lvT, lvl * 4}, {&p.o_lvV, lvl * 4},  {&p.o_lvK, lvl * 4},
+      {&p.o_lvM, lvl * wpl * 4},
   };
   if (greedy || ovl) {
     items.push_back({&p.o_cls, 5LL * (S + 2) * 4});  // int4 records + int32 starts
     items.push_back({&p.o_bm, bm_words * 8});
     items.push_back({&p.o_pbm, bm_words * 8});
   }
+  if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8});
+  if (greedy && H > 0) items.push_back({&p.o_M, std::max<int64_t>((H + 1) * 8LL, 128)});  // + register-chain row
+  if (g.noisy) items.push_back({&p.o_mt, 312 * 8});
+  items.push_back({&p.o_rl, 32LL * rstride * 4});
+  if (!p.cal) items.push_back({&p.o_rlist, GB * 2});
+  for (Item it : std::initializer_list<Item>{{&p.o_f, ((GB + 3) & ~3LL) * 4}, {&p.o_stk, GB * 2},
+                                             {&p.o_a, GB * 4}, {&p.o_x, GB * 4}, {&p.o_id, GB * 4}})
+    items.push_back(it);
   items.push_back({&p.o_stage, GB * 8});
   if (greedy && H > 0) {
-    items.push_back({&p.o_M, std::max<int64_t>((H + 1) * 8LL, 128)});  // also the register chain row
     items.push_back({&p.o_F, (H + 1) * 8LL * G});
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
   }
-  p.noisy = g.noisy;
   if (g.noisy) {
-    items.push_back({&p.o_mt, 312 * 8});
     items.push_back({&p.o_lst, GB * 2});
     items.push_back({&p.o_onz, GB * 4});
   }
-  if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8});
   if (greedy) {
     items.push_back({&p.o_res, GB * 4});
     items.push_back({&p.o_pcl, GB * 4});
@@ -253,13 +263,11 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
       items.push_back({&p.o_oid, GB * 4});
     }
   }
-  p.cbuf = static_cast<int>(std::min<int64_t>(GB + 512, 1 << 24));
-  items.push_back({&p.o_misc, 16});
   int64_t sm_off = 0, ws_off = 0;
   int spilled = 0;
   for (auto& it : items) {
     int64_t b = (it.bytes + 15) & ~15LL;
-    if (!spilled && sm_off + b <= smem_budget) {
+    if (sm_off + b <= smem_budget) {
       *it.code = sm_off;
       sm_off += b;
     } else {
@@ -278,9 +286,6 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   };
   cold(&p.o_ring, R * 8LL);
   cold(&p.o_cbuf, static_cast<int64_t>(p.cbuf) * 8);
-  // completion calendar instead of the per-step finish-step scan once the
-  // slot arrays outgrow shared memory
-  p.cal = GB > 4096 ? 1 : 0;
   if (p.cal) {
     cold(&p.o_calh, static_cast<int64_t>(R) * 32 * 4);
     cold(&p.o_calnx, GB * 4);

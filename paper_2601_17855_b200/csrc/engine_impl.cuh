@@ -946,10 +946,53 @@ BFSIM_UNROLL_W
     }
     if (SM) cp_async_wait_all();
     __syncwarp();
-    // placement, segment by segment: level l, worker block j holds the
-    // next min(popc, left) admissions in worker-index order; admission t
-    // takes waiting request head + t
-    {
+    // placement: admission t takes waiting request head + t and goes to the
+    // worker it is the t-th of, levels in order, index order within a level
+    auto fifo_place = [&](int t, int g, int vl) {
+      const int rank = JSQ ? vl - (B - s_capb[g]) : s_capb[g] - vl;
+      const long long id = head + t;
+      int s, o;
+      if (SM && t < umax) {
+        int2 v = stage[t];
+        s = v.x;
+        o = v.y;
+      } else if (OVL) {
+        int2 v = __ldg(reinterpret_cast<const int2*>(st) + id);
+        s = v.x;
+        o = v.y;
+      } else {
+        int4 v = __ldg(reinterpret_cast<const int4*>(tr) + id);
+        s = v.z;
+        o = v.w;
+      }
+      if (OVL) atomicAdd(&c_rec[s].x, 1);  // leaves the pool (class count for Def. 1)
+      place(g, rank, id, s, o);
+      atomicAdd(&s_asum[g], static_cast<unsigned long long>(static_cast<long long>(s) - d * k));
+    };
+    if constexpr (WPL <= 2) {
+      // item-parallel: few worker blocks, so each lane finds its level and
+      // worker directly
+      for (int t = lane; t < U; t += 32) {
+        int l = 0;
+        while (l + 1 < nl && lvT[l + 1] <= t) ++l;
+        int pos = t - lvT[l];
+        int g = 0;
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          const uint32_t mk = lvM[l * WPL + j];
+          const int c = __popc(mk);
+          if (pos >= 0 && pos < c) {
+            g = static_cast<int>(__fns(mk, 0, pos + 1)) + 32 * j;
+            pos = -1;
+          } else if (pos >= 0) {
+            pos -= c;
+          }
+        }
+        fifo_place(t, g, lvV[l]);
+      }
+    } else {
+      // segment by segment: level l, worker block j holds the next
+      // min(popc, left) admissions
       int t0 = 0;
       for (int l = 0; l < nl; ++l) {
         int left = lvK[l];
@@ -958,29 +1001,8 @@ BFSIM_UNROLL_W
           const uint32_t mk = lvM[l * WPL + j];
           int c = __popc(mk);
           c = c < left ? c : left;
-          for (int i = lane; i < c; i += 32) {
-            const int g = static_cast<int>(__fns(mk, 0, i + 1)) + 32 * j;
-            const int t = t0 + i;
-            const int rank = JSQ ? vl - (B - s_capb[g]) : s_capb[g] - vl;
-            const long long id = head + t;
-            int s, o;
-            if (SM && t < umax) {
-              int2 v = stage[t];
-              s = v.x;
-              o = v.y;
-            } else if (OVL) {
-              int2 v = __ldg(reinterpret_cast<const int2*>(st) + id);
-              s = v.x;
-              o = v.y;
-            } else {
-              int4 v = __ldg(reinterpret_cast<const int4*>(tr) + id);
-              s = v.z;
-              o = v.w;
-            }
-            if (OVL) atomicAdd(&c_rec[s].x, 1);  // leaves the pool (class count for Def. 1)
-            place(g, rank, id, s, o);
-            atomicAdd(&s_asum[g], static_cast<unsigned long long>(static_cast<long long>(s) - d * k));
-          }
+          for (int i = lane; i < c; i += 32)
+            fifo_place(t0 + i, static_cast<int>(__fns(mk, 0, i + 1)) + 32 * j, vl);
           t0 += c;
           left -= c;
         }
