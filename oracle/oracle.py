@@ -176,6 +176,8 @@ class RefLib:
         L.ref_estimate_iir.argtypes = [_vp, C.c_int, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _f64, _i64, _f64, _f64, _f64, _f64, C.c_int, _i64, _i64, _u64, _vp, _vp, C.c_size_t]
         L.ref_bench_poisson.argtypes = [_vp, _i64, _vp, _vp, C.c_int, _vp]
         L.ref_bench_poisson.restype = _f64
+        L.ref_bench_overloaded.argtypes = [_vp, _i64, C.c_int, C.c_int, C.c_int, _f64, _i64, C.c_int, _vp]
+        L.ref_bench_overloaded.restype = _f64
 
     def sample_instance(self, s_max=64, p=0.02, rate=50.0, duration=10.0, seed=0,
                         prefill_kind=0, decode_kind=0, fixed_o=1):
@@ -264,6 +266,13 @@ class RefLib:
         if rc:
             raise ValueError(err.value.decode())
         return out
+
+    def bench_overloaded(self, scen, threads, s_max=64, p=0.02, prefill_kind=0, decode_kind=0, fixed_o=1):
+        scen = np.ascontiguousarray(scen, abi.scenario_dtype)
+        ws = np.zeros(1, np.int64)
+        sec = self.lib.ref_bench_overloaded(abi.ptr(scen), scen.shape[0], prefill_kind, s_max, decode_kind, p,
+                                            fixed_o, threads, abi.ptr(ws))
+        return sec, int(ws[0])
 
     def bench_poisson(self, scen, inputs, traces, threads):
         scen = np.ascontiguousarray(scen, abi.scenario_dtype)

@@ -354,4 +354,49 @@ double ref_bench_poisson(const bfsim_scenario_t* scen, int64_t n_scen, const bfs
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+
+// CPU baseline for run_overloaded (oracle.hpp:138-244) + compute_metrics:
+// each scenario runs the reference loop, drawing its own samples from
+// mt19937_64(seed); one scenario per task on `threads` host threads.
+// Returns wall seconds; worker_steps receives sum of G * (warmup + steps).
+double ref_bench_overloaded(const bfsim_scenario_t* scen, int64_t n_scen, int prefill_kind, int s_max,
+                            int decode_kind, double p, int64_t fixed_o, int threads,
+                            int64_t* worker_steps) {
+  std::atomic<int64_t> next{0}, ws{0};
+  auto body = [&]() {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n_scen) break;
+      const bfsim_scenario_t& sc = scen[i];
+      bfsim::OverloadedSpec spec;
+      spec.prefill = make_prefill(prefill_kind, s_max);
+      spec.decode = make_decode(decode_kind, p, fixed_o);
+      spec.drift = bfsim::DriftSpec::constant(sc.drift);
+      spec.overhead = sc.overhead;
+      spec.per_token = sc.per_token;
+      spec.backlog = sc.backlog;
+      bfsim::PowerModel power;
+      power.p_idle = sc.p_idle;
+      power.p_max = sc.p_max;
+      power.mfu_sat = sc.mfu_sat;
+      power.gamma = sc.gamma;
+      std::vector<bfsim::RequestTiming> timings;
+      auto steps = bfsim::run_overloaded(static_cast<bfsim::PolicyKind>(sc.policy), sc.horizon,
+                                         sc.workers, sc.batch, sc.steps, sc.warmup, spec, sc.seed,
+                                         200000, &timings);
+      volatile double sink = 0.0;
+      if (!steps.empty()) sink = bfsim::compute_metrics(steps, timings, power).avg_imbalance;
+      (void)sink;
+      ws.fetch_add(static_cast<int64_t>(sc.steps + sc.warmup) * sc.workers);
+    }
+  };
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(body);
+  for (auto& t : pool) t.join();
+  auto t1 = std::chrono::steady_clock::now();
+  *worker_steps = ws.load();
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
 }  // extern "C"

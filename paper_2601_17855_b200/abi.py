@@ -12,6 +12,7 @@ OK, EINVAL, ELOGIC, ECUDA, PARTIAL, ESTREAM = 0, 1, 2, 3, 4, 5
 # PolicyKind, policies.hpp:16
 FCFS, JSQ, BFIO_EXACT, BFIO_GREEDY = 0, 1, 2, 3
 POLICY_NAMES = {"fcfs": FCFS, "jsq": JSQ, "bfio-exact": BFIO_EXACT, "bfio-greedy": BFIO_GREEDY}
+POLICY_LABELS = {v: k for k, v in POLICY_NAMES.items()}
 # LookaheadMode, policies.hpp:36
 PERFECT, TRUNCATED, NOISY = 0, 1, 2
 POISSON, OVERLOADED = 0, 1

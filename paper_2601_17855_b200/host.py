@@ -373,7 +373,7 @@ class PinnedBatch:
     page-locked host buffers (inputs copied H2D and all outputs D2H inside
     every call)."""
 
-    def __init__(self, ctx: Context, scen, pool: InputPool, *, step_capacity, emit_requests=True):
+    def __init__(self, ctx: Context, scen, pool: InputPool, *, step_capacity=None, emit_requests=True):
         import torch
 
         def pinned(n, dtype):
@@ -384,7 +384,9 @@ class PinnedBatch:
         self._keep = []
         self.ctx = ctx
         scen = np.array(scen, abi.scenario_dtype, copy=True).reshape(-1)
-        caps = np.asarray(step_capacity, np.int64).reshape(-1)
+        # step_capacity None: metrics and request timings only (no StepRecord sink)
+        caps = (np.zeros(scen.shape[0], np.int64) if step_capacity is None
+                else np.asarray(step_capacity, np.int64).reshape(-1))
         scen["step_capacity"] = caps
         scen["step_offset"] = np.concatenate([[0], np.cumsum(caps)[:-1]])
         lcaps = caps * scen["workers"]
@@ -402,10 +404,12 @@ class PinnedBatch:
         self.is_stream = pool.kind == "stream"
         self.records = pinned(pool.records.shape[0], pool.records.dtype)
         self.records[:] = pool.records
-        self.steps = {k: pinned(self.nrec, np.float64) for k in ("clock_start", "dt", "max_load")}
-        self.steps["active_count"] = pinned(self.nrec, np.int64)
-        self.steps["loads"] = pinned(max(1, self.nload), np.float64)
-        self.sink_s = _StepSink(*[abi.ptr(self.steps[k]) for k in ("clock_start", "dt", "max_load", "active_count", "loads")])
+        self.steps, self.sink_s = {}, None
+        if step_capacity is not None:
+            self.steps = {k: pinned(self.nrec, np.float64) for k in ("clock_start", "dt", "max_load")}
+            self.steps["active_count"] = pinned(self.nrec, np.int64)
+            self.steps["loads"] = pinned(max(1, self.nload), np.float64)
+            self.sink_s = _StepSink(*[abi.ptr(self.steps[k]) for k in ("clock_start", "dt", "max_load", "active_count", "loads")])
         self.sink_r = None
         if emit_requests:
             self.reqs = {k: pinned(self.nreq, np.int32) for k in ("arrival_step", "start_step", "worker")}
@@ -432,7 +436,7 @@ class PinnedBatch:
             abi.ptr(self.class_base), self.class_base.shape[0],
             None if st else abi.ptr(self.records), 0 if st else self.records.shape[0],
             abi.ptr(self.records) if st else None, self.records.shape[0] if st else 0,
-            C.byref(self.sink_s), self.nrec, self.nload,
+            C.byref(self.sink_s) if self.sink_s is not None else None, self.nrec, self.nload,
             C.byref(self.sink_r) if self.sink_r is not None else None, self.nreq,
             abi.ptr(self.results), err, 1024,
         )
