@@ -171,6 +171,7 @@ int wpl_for(int G) {
 
 struct Group {
   int mode, policy, wpl, small, noisy, hr;
+  int64_t hot_bytes = 0;
   std::vector<int32_t> idx;
   Plan plan;
   int wpc = 4, grid = 0;
@@ -236,23 +237,27 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_pbm, bm_words * 8});
   }
   if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8});
-  if (greedy && H > 0) items.push_back({&p.o_M, std::max<int64_t>((H + 1) * 8LL, 128)});  // + register-chain row
+  // M, T, w of the lookahead chain (also the register chain's row)
+  if (greedy && H > 0) items.push_back({&p.o_M, std::max<int64_t>(3 * (H + 1) * 8LL, 128)});
   if (g.noisy) items.push_back({&p.o_mt, 312 * 8});
-  items.push_back({&p.o_rl, 32LL * rstride * 4});
-  if (!p.cal) items.push_back({&p.o_rlist, GB * 2});
-  for (Item it : std::initializer_list<Item>{{&p.o_f, ((GB + 3) & ~3LL) * 4}, {&p.o_stk, GB * 2},
-                                             {&p.o_a, GB * 4}, {&p.o_x, GB * 4}, {&p.o_id, GB * 4}})
-    items.push_back(it);
-  items.push_back({&p.o_stage, GB * 8});
+  // per-slot state touched every step (retire scan, noisy views)
+  items.push_back({&p.o_f, ((GB + 3) & ~3LL) * 4});
+  items.push_back({&p.o_a, GB * 4});
+  if (g.noisy) items.push_back({&p.o_lst, GB * 2});
+  items.push_back({&p.o_stk, GB * 2});
   if (greedy && H > 0) {
     items.push_back({&p.o_F, (H + 1) * 8LL * G});
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
   }
-  if (g.noisy) {
-    items.push_back({&p.o_lst, GB * 2});
-    items.push_back({&p.o_onz, GB * 4});
-  }
+  if (!p.cal) items.push_back({&p.o_rlist, GB * 2});
+  const size_t n_hot = items.size();  // the residency planner tries to keep these in shared memory
+  items.push_back({&p.o_id, GB * 4});
+  items.push_back({&p.o_x, GB * 4});
+  items.push_back({&p.o_rl, 32LL * rstride * 4});
+  // per-admission scratch (sized for the worst step, touched U times a step)
+  items.push_back({&p.o_stage, GB * 8});
+  if (g.noisy) items.push_back({&p.o_onz, GB * 4});
   if (greedy) {
     items.push_back({&p.o_res, GB * 4});
     items.push_back({&p.o_pcl, GB * 4});
@@ -263,6 +268,9 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
       items.push_back({&p.o_oid, GB * 4});
     }
   }
+  int64_t hot = 0;
+  for (size_t i = 0; i < n_hot; ++i) hot += (items[i].bytes + 15) & ~15LL;
+  g.hot_bytes = hot;
   int64_t sm_off = 0, ws_off = 0;
   int spilled = 0;
   for (auto& it : items) {
@@ -430,8 +438,15 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     // to hold every group of the batch at once (the groups run concurrently
     // and the warps are latency-bound); what does not fit spills to the
     // per-warp global workspace (generic-addressing kernel variant)
+    // Residency: enough trajectories per SM for the whole batch, but never
+    // so many that the per-step working set (the planner's hot arrays)
+    // leaves shared memory -- a latency-bound warp that misses to L2 on every
+    // slot access is slower than a second wave of warps that do not.
     int64_t per_sm = (n_scen + ctx->sm_count - 1) / ctx->sm_count;
     per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, 16));
+    make_plan(g, scen_host, inputs_host, 1 << 30);  // dry run: size of the hot set
+    const int64_t fit = (228 * 1024) / (g.hot_bytes + 2048 + 1024);
+    per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, fit));
     int budget = static_cast<int>(std::min<int64_t>(ctx->smem_optin - 1024,
                                                     (228 * 1024) / per_sm - 2048));
     budget = std::max(budget, 8 * 1024);

@@ -1437,10 +1437,21 @@ BFSIM_UNROLL_W
         }
         __syncwarp();
       } else {
-        for (int h = lane; h <= H; h += 32) {
+        // Shared-memory chain (any G and H): the same cost split as the
+        // register chain -- sum_h max(T_h, F_h[g]) with T_h = M_h - w_h per
+        // item in shared memory -- and the chosen row / maxima updated by all
+        // lanes in parallel over h.
+        long long* s_T = s_M + (H + 1);
+        long long* s_w = s_M + 2 * (H + 1);
+        for (int h = 0; h <= H; ++h) {
           long long m = 0;
-          for (int g = 0; g < G; ++g) m = s_F[h * G + g] > m ? s_F[h * G + g] : m;
-          s_M[h] = m;
+          for (int g = lane; g < G; g += 32) m = s_F[h * G + g] > m ? s_F[h * G + g] : m;
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const long long t = __shfl_xor_sync(FULLMASK, m, off);
+            m = t > m ? t : m;
+          }
+          if (lane == 0) s_M[h] = m;
         }
         __syncwarp();
         for (int q = 0; q < U; ++q) {
@@ -1455,47 +1466,71 @@ BFSIM_UNROLL_W
           } else {
             if (trunc && lim < H + 1) lim = H + 1;
           }
+          for (int h = lane; h <= H; h += 32) {
+            const long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
+            s_w[h] = w;
+            s_T[h] = s_M[h] - w;
+          }
+          __syncwarp();
           // lane-best (cost, F0, g) over owned workers with a free slot
           uint64_t bc = ~0ull, bk = ~0ull;
   BFSIM_UNROLL_W
           for (int j = 0; j < WPL; ++j) {
-            int g = lane + 32 * j;
+            const int g = lane + 32 * j;
             if (g >= G || cp[j] <= 0) continue;
-            long long cost = 0;
-            for (int h = 0; h <= H; ++h) {
-              long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
-              long long v = s_F[h * G + g] + w;
-              long long m = s_M[h];
-              cost += v > m ? v : m;
+            long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            int h = 0;
+            for (; h + 3 <= H; h += 4) {
+              const long long f0 = s_F[h * G + g], f1 = s_F[(h + 1) * G + g];
+              const long long f2 = s_F[(h + 2) * G + g], f3 = s_F[(h + 3) * G + g];
+              const long long t0 = s_T[h], t1 = s_T[h + 1], t2 = s_T[h + 2], t3 = s_T[h + 3];
+              a0 += t0 > f0 ? t0 : f0;
+              a1 += t1 > f1 ? t1 : f1;
+              a2 += t2 > f2 ? t2 : f2;
+              a3 += t3 > f3 ? t3 : f3;
             }
-            uint64_t k2 = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
-            if (static_cast<uint64_t>(cost) < bc || (static_cast<uint64_t>(cost) == bc && k2 < bk)) {
-              bc = static_cast<uint64_t>(cost);
+            for (; h <= H; ++h) {
+              const long long f0 = s_F[h * G + g], t0 = s_T[h];
+              a0 += t0 > f0 ? t0 : f0;
+            }
+            const uint64_t cost = static_cast<uint64_t>(a0 + a1 + a2 + a3);
+            const uint64_t k2 = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
+            if (cost < bc || (cost == bc && k2 < bk)) {
+              bc = cost;
               bk = k2;
             }
           }
-          uint64_t cmin = wmin_u64(bc);
-          uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
-          int gs = static_cast<int>(kmin & gmask);
-  BFSIM_UNROLL_W
-          for (int j = 0; j < WPL; ++j)
-            if (lane + 32 * j == gs) {
-              for (int h = 0; h <= H; ++h) {
-                long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
-                long long v = s_F[h * G + gs] + w;
-                s_F[h * G + gs] = v;
-                if (v > s_M[h]) s_M[h] = v;
-              }
-              cp[j] -= 1;
-              A[j] += c + ak;
-              s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
-              adm[j] += 1;
-              if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
-                int r = static_cast<int>((k + o - 1) % Hm);
-                s_Wc[r * G + gs] += 1;
-                s_Wa[r * G + gs] += c + ak;
-              }
+          const uint64_t cmin = wmin_u64(bc);
+          const uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
+          const int gs = static_cast<int>(kmin & gmask);
+          for (int h = lane; h <= H; h += 32) {
+            const long long v = s_F[h * G + gs] + s_w[h];
+            s_F[h * G + gs] = v;
+            if (v > s_M[h]) s_M[h] = v;
+          }
+          if (lane == (gs & 31)) {
+            const int jj = gs >> 5;
+            if constexpr (WPL > 8) {
+              cp[jj] -= 1;
+              A[jj] += c + ak;
+              s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[jj]) << 16);
+              adm[jj] += 1;
+            } else {
+#pragma unroll
+              for (int j = 0; j < WPL; ++j)
+                if (j == jj) {
+                  cp[j] -= 1;
+                  A[j] += c + ak;
+                  s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
+                  adm[j] += 1;
+                }
             }
+            if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
+              const int r = static_cast<int>((k + o - 1) % Hm);
+              s_Wc[r * G + gs] += 1;
+              s_Wa[r * G + gs] += c + ak;
+            }
+          }
           __syncwarp();
         }
       }

@@ -443,3 +443,72 @@ class PinnedBatch:
         if rc not in (abi.OK, abi.PARTIAL):
             _raise(rc, err)
         return self.results
+
+
+def run_overloaded_batch(ctx: Context, jobs, *, s_max=64, p=0.02, drift=0.0, prefill_kind=0, decode_kind=0,
+                         fixed_o=1, backlog=1.0, overhead=9.775e-3, per_token=1.005e-7, emit_steps=False,
+                         emit_requests=False):
+    """run_overloaded (oracle.hpp:138-244) for many jobs in one batch.
+
+    jobs: iterable of (policy, H, G, B, steps, warmup, seed). Each job's
+    (prefill, decode) draws from mt19937_64(seed) are pre-generated here
+    (bfsim_sample_stream; policy-independent) and shared by the
+    jobs with the same seed. A stream that runs dry (code 5) is doubled and
+    the batch re-run, so callers see the reference's unbounded top-up.
+    Returns (BatchResult, streams by seed)."""
+    jobs = list(jobs)
+    mean_o = 1.0 / p if decode_kind == 0 else float(fixed_o)
+    need = {}
+    for (_, _, G, B, steps, warmup, seed) in jobs:
+        n = int(G * B * (3 + (steps + warmup) / mean_o * 1.5)) + 4096
+        need[seed] = max(need.get(seed, 0), n)
+    streams = {}
+    for _ in range(12):
+        for seed, n in need.items():
+            if seed not in streams or streams[seed].shape[0] < n:
+                streams[seed] = sample_stream(seed, n, s_max=s_max, p=p, prefill_kind=prefill_kind,
+                                              decode_kind=decode_kind, fixed_o=fixed_o)
+        order = list(need)
+        pool = InputPool([streams[s] for s in order])
+        # the class structures cover the distribution's whole range
+        pos = {s: i for i, s in enumerate(order)}
+        scen = np.array([scenario(mode=abi.OVERLOADED, policy=pol, horizon=H, workers=G, batch=B, steps=steps,
+                                  warmup=warmup, seed=seed, drift=drift, backlog=backlog, overhead=overhead,
+                                  per_token=per_token, input_id=pos[seed])
+                         for (pol, H, G, B, steps, warmup, seed) in jobs], abi.scenario_dtype)
+        try:
+            br = ctx.run_batch(scen, pool, emit_steps=emit_steps, emit_requests=emit_requests)
+            return br, streams
+        except BfsimError as e:
+            if e.code != abi.ESTREAM:
+                raise
+        for seed in need:  # a stream ran dry: grow them all and re-run
+            need[seed] *= 2
+    raise BfsimError(abi.ESTREAM, "overloaded sample stream still exhausted after 12 doublings")
+
+
+def estimate_iir(ctx: Context, batch_sizes, worker_counts, trials, steps, warmup, seed, *, s_max=64, p=0.02,
+                 drift=0.0, backlog=1.0, overhead=9.775e-3, per_token=1.005e-7):
+    """estimate_iir (oracle.hpp:263-317) on the GPU: every (B, G, trial) x
+    {FCFS, BF-IO greedy H=0} trajectory in one batch, trial seed
+    seed + 1000003*t + 17*B + G (oracle.hpp:279-281), reduced with the
+    reference formulas (bfsim_iir_reduce). Returns rows
+    [B, G, fcfs_mean, bfio_mean, ratio, stderr, trials, outside_regime]."""
+    if trials < 1:
+        raise InvalidArgument(abi.EINVAL, "estimate_iir: trials must be >= 1")
+    jobs, cells = [], []
+    for B in batch_sizes:
+        for G in worker_counts:
+            cells.append((B, G))
+            for t in range(trials):
+                ts = (seed + 1000003 * t + 17 * B + G) & ((1 << 64) - 1)
+                jobs.append((abi.FCFS, 0, G, B, steps, warmup, ts))
+                jobs.append((abi.BFIO_GREEDY, 0, G, B, steps, warmup, ts))
+    br, _ = run_overloaded_batch(ctx, jobs, s_max=s_max, p=p, drift=drift, backlog=backlog, overhead=overhead,
+                                 per_token=per_token)
+    m = br.res["avg_imbalance"].reshape(len(cells), trials, 2)
+    red = iir_reduce(m[:, :, 0], m[:, :, 1])
+    out = np.zeros((len(cells), 8))
+    for c, (B, G) in enumerate(cells):
+        out[c] = [B, G, red[c, 0], red[c, 1], red[c, 2], red[c, 3], trials, float(np.sqrt(G) > B)]
+    return out

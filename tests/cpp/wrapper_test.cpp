@@ -6,6 +6,7 @@
 // check; exit code = number of failures. Needs a B200 (run from pytest -m gpu).
 #include <cstdio>
 #include <random>
+#include <sstream>
 #include <string>
 
 #include "bfsim/engine.hpp"
@@ -127,7 +128,9 @@ int main() {
       SimConfig c = small(G, B, std::vector<PolicyKind>{PolicyKind::Fcfs, PolicyKind::Jsq,
                                                         PolicyKind::BfioGreedy}[rng() % 3]);
       c.horizon = std::vector<int>{0, 0, 1, 4, 20}[rng() % 5];
-      c.lookahead = (rng() % 2) ? LookaheadMode::Perfect : LookaheadMode::TruncatedAtH;
+      c.lookahead = std::vector<LookaheadMode>{LookaheadMode::Perfect, LookaheadMode::TruncatedAtH,
+                                               LookaheadMode::Noisy}[rng() % 3];
+      c.noise_sigma = std::vector<double>{0.5, 2.0, 7.0}[rng() % 3];
       c.seed = rng();
       double drift = static_cast<double>(rng() % 3);
       auto inst = sample_instance(PrefillDistribution::uniform(2 + static_cast<int>(rng() % 100)),
@@ -142,7 +145,7 @@ int main() {
     auto gres = gpu::run_batch(ctx, cfgs, ptrs);
     bool ok = true;
     for (size_t i = 0; i < cfgs.size(); ++i) ok = ok && same_result(gres[i], run(cfgs[i], insts[i]));
-    report("gpu::run_batch == bfsim::run (40 random trajectories)", ok);
+    report("gpu::run_batch == bfsim::run (40 random trajectories, perfect/truncated/noisy)", ok);
   }
   {  // oracle_test.cpp:99-107
     OverloadedSpec spec;
@@ -196,6 +199,35 @@ int main() {
            g.cells[c].ratio == r.cells[c].ratio && g.cells[c].stderr_ == r.cells[c].stderr_ &&
            g.cells[c].outside_regime == r.cells[c].outside_regime;
     report("gpu::estimate_iir == estimate_iir (2x2 grid, 4 trials)", ok);
+  }
+  {  // the reference's own writers over GPU results are
+     // byte-identical (steps.csv engine.hpp:270-281, summary metrics.hpp:129-136,
+     // iir.csv oracle.hpp:321-330) -- the adapter returns the reference's types
+    auto inst = sample_instance(PrefillDistribution::uniform(64), DecodeDistribution::geometric(0.02), 2000.0,
+                                1.0, 1, DriftSpec::unit());
+    bool ok = true;
+    for (PolicyKind p : {PolicyKind::Fcfs, PolicyKind::BfioGreedy}) {
+      SimConfig c = small(8, 64, p);
+      c.horizon = p == PolicyKind::BfioGreedy ? 20 : 0;
+      c.lookahead = LookaheadMode::Noisy;
+      c.noise_sigma = 2.0;
+      c.seed = 5;
+      SimResult g = gpu::run(ctx, c, inst), r = run(c, inst);
+      std::ostringstream a, b;
+      write_step_csv(a, g);
+      write_summary(a, compute_metrics(g));
+      write_step_csv(b, r);
+      write_summary(b, compute_metrics(r));
+      ok = ok && a.str() == b.str();
+    }
+    OverloadedSpec spec;
+    spec.prefill = PrefillDistribution::uniform(16);
+    spec.decode = DecodeDistribution::geometric(0.1);
+    std::ostringstream a, b;
+    write_iir_csv(a, gpu::estimate_iir(ctx, {2, 8}, {2, 16}, spec, 3, 80, 20, 9));
+    write_iir_csv(b, estimate_iir({2, 8}, {2, 16}, spec, 3, 80, 20, 9));
+    ok = ok && a.str() == b.str();
+    report("write_step_csv / write_summary / write_iir_csv byte-identical (C1, noisy H=20)", ok);
   }
   {  // acceptance_test.cpp:178-180 (C04) through the GPU path
     OverloadedSpec spec;
