@@ -59,6 +59,9 @@ struct bfsim_ctx {
   DevBuf order, ws, queue;
   int64_t last_launches = 0;
   bool timed = false;
+  // residency policy: 0 = as many trajectories per SM as the batch needs
+  // (measured best on C3); 1 = cap it so the hot arrays stay in shared memory
+  int fit_hot = 0;
 };
 
 namespace {
@@ -444,9 +447,11 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     // slot access is slower than a second wave of warps that do not.
     int64_t per_sm = (n_scen + ctx->sm_count - 1) / ctx->sm_count;
     per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, 16));
-    make_plan(g, scen_host, inputs_host, 1 << 30);  // dry run: size of the hot set
-    const int64_t fit = (228 * 1024) / (g.hot_bytes + 2048 + 1024);
-    per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, fit));
+    if (ctx->fit_hot) {
+      make_plan(g, scen_host, inputs_host, 1 << 30);  // dry run: size of the hot set
+      const int64_t fit = (228 * 1024) / (g.hot_bytes + 2048 + 1024);
+      per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, fit));
+    }
     int budget = static_cast<int>(std::min<int64_t>(ctx->smem_optin - 1024,
                                                     (228 * 1024) / per_sm - 2048));
     budget = std::max(budget, 8 * 1024);

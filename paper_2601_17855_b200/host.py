@@ -472,7 +472,7 @@ def run_overloaded_batch(ctx: Context, jobs, *, s_max=64, p=0.02, drift=0.0, pre
         pool = InputPool([streams[s] for s in order])
         # the class structures cover the distribution's whole range
         pos = {s: i for i, s in enumerate(order)}
-        scen = np.array([scenario(mode=abi.OVERLOADED, policy=pol, horizon=H, workers=G, batch=B, steps=steps,
+        scen = np.array([abi.scenario(mode=abi.OVERLOADED, policy=pol, horizon=H, workers=G, batch=B, steps=steps,
                                   warmup=warmup, seed=seed, drift=drift, backlog=backlog, overhead=overhead,
                                   per_token=per_token, input_id=pos[seed])
                          for (pol, H, G, B, steps, warmup, seed) in jobs], abi.scenario_dtype)
