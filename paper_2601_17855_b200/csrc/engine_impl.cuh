@@ -1373,7 +1373,6 @@ BFSIM_UNROLL_W
           const int32_t m = static_cast<int32_t>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(v)));
           Ml = lane == h ? m : Ml;
         }
-        int32_t* s_row = reinterpret_cast<int32_t*>(s_M);  // the chosen worker's new F_h row
         const int32_t d32 = static_cast<int32_t>(d);
         const int32_t dl = d32 * lane;
         for (int q = 0; q < U; ++q) {
@@ -1389,14 +1388,12 @@ BFSIM_UNROLL_W
           const int32_t sat = d32 * (o - 1);
           const int32_t wl = lane < limH ? c + (dl < sat ? dl : sat) : 0;
           const int32_t Tl = Ml - wl;
-          int32_t wv[HR];
           uint32_t cost[WPL];
 #pragma unroll
           for (int j = 0; j < WPL; ++j) cost[j] = 0;
 #pragma unroll
           for (int h = 0; h < HR; ++h) {
             const int32_t T = __shfl_sync(FULLMASK, Tl, h);
-            wv[h] = __shfl_sync(FULLMASK, wl, h);
 #pragma unroll
             for (int j = 0; j < WPL; ++j) cost[j] += static_cast<uint32_t>(T > Fr[j][h] ? T : Fr[j][h]);
           }
@@ -1411,15 +1408,21 @@ BFSIM_UNROLL_W
           }
           const uint64_t km = wmin_u64(best);
           const int gs = static_cast<int>(km & gmask);
-          if (lane == (gs & 31)) {
+          const int own = gs & 31, jj = gs >> 5;
+          // the chosen row gains w_h (broadcast from lane h); lane h then
+          // raises M_h with the row's new value (broadcast from the owner)
+#pragma unroll
+          for (int h = 0; h < HR; ++h) {
+            const int32_t w = __shfl_sync(FULLMASK, wl, h);
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) Fr[j][h] += (lane == own && j == jj) ? w : 0;
+            const int32_t nv = __shfl_sync(FULLMASK, (WPL > 1 && jj) ? Fr[WPL - 1][h] : Fr[0][h], own);
+            Ml = (lane == h && nv > Ml) ? nv : Ml;
+          }
+          if (lane == own) {
 #pragma unroll
             for (int j = 0; j < WPL; ++j)
-              if (j == (gs >> 5)) {
-#pragma unroll
-                for (int h = 0; h < HR; ++h) {
-                  Fr[j][h] += wv[h];
-                  s_row[h] = Fr[j][h];
-                }
+              if (j == jj) {
                 cp[j] -= 1;
                 A[j] += c + ak;
                 s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
@@ -1431,9 +1434,6 @@ BFSIM_UNROLL_W
                 }
               }
           }
-          __syncwarp();
-          if (lane < HR) Ml = s_row[lane] > Ml ? s_row[lane] : Ml;
-          __syncwarp();
         }
         __syncwarp();
       } else {

@@ -14,13 +14,14 @@ from paper_2601_17855_b200 import abi, host
 which = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 if which.startswith("c4"):
-    G = 1024
+    G = 256 if "g256" in which else 1024
     pol = abi.FCFS if which == "c4fcfs" else abi.BFIO_GREEDY
+    H, drift = (20, 1.0) if "h20" in which else (0, 0.0)
     steps, warm = 150, 50
     ln = int(G * 64 * (2 + (steps + warm) * 0.02 * 1.3)) + 4096
     inputs = [host.sample_stream(s, ln, s_max=64, p=0.02) for s in range(1, n + 1)]
     scs = [abi.scenario(mode=abi.OVERLOADED, policy=pol, workers=G, batch=64, steps=steps, warmup=warm, seed=s,
-                        input_id=i) for i, s in enumerate(range(1, n + 1))]
+                        horizon=H, drift=drift, input_id=i) for i, s in enumerate(range(1, n + 1))]
 elif which.startswith("c3"):
     noisy = which == "c3noisy"
     inputs = [host.sample_instance(s, rate=8000.0, duration=2.0, s_max=64, p=0.02) for s in range(1, n + 1)]
