@@ -1472,37 +1472,54 @@ BFSIM_UNROLL_W
             s_T[h] = s_M[h] - w;
           }
           __syncwarp();
-          // lane-best (cost, F0, g) over owned workers with a free slot
-          uint64_t bc = ~0ull, bk = ~0ull;
+          // Fast path: g* = argmin (F_0[g], g) over workers with a free slot.
+          // Its excess sum_h max(0, F_h[g*] - T_h) is 0 iff no horizon rises
+          // above the current maximum; every cost is >= sum_h T_h, so then g*
+          // wins outright (cost and tie-break). Otherwise the full scan.
+          uint64_t fk = ~0ull;
   BFSIM_UNROLL_W
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
-            if (g >= G || cp[j] <= 0) continue;
-            long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-            int h = 0;
-            for (; h + 3 <= H; h += 4) {
-              const long long f0 = s_F[h * G + g], f1 = s_F[(h + 1) * G + g];
-              const long long f2 = s_F[(h + 2) * G + g], f3 = s_F[(h + 3) * G + g];
-              const long long t0 = s_T[h], t1 = s_T[h + 1], t2 = s_T[h + 2], t3 = s_T[h + 3];
-              a0 += t0 > f0 ? t0 : f0;
-              a1 += t1 > f1 ? t1 : f1;
-              a2 += t2 > f2 ? t2 : f2;
-              a3 += t3 > f3 ? t3 : f3;
-            }
-            for (; h <= H; ++h) {
-              const long long f0 = s_F[h * G + g], t0 = s_T[h];
-              a0 += t0 > f0 ? t0 : f0;
-            }
-            const uint64_t cost = static_cast<uint64_t>(a0 + a1 + a2 + a3);
-            const uint64_t k2 = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
-            if (cost < bc || (cost == bc && k2 < bk)) {
-              bc = cost;
-              bk = k2;
-            }
+            const uint64_t key = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
+            if (g < G && cp[j] > 0 && key < fk) fk = key;
           }
-          const uint64_t cmin = wmin_u64(bc);
-          const uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
-          const int gs = static_cast<int>(kmin & gmask);
+          const int gstar = static_cast<int>(wmin_u64(fk) & gmask);
+          bool over = false;
+          for (int h = lane; h <= H; h += 32) over = over || s_F[h * G + gstar] > s_T[h];
+          int gs = gstar;
+          if (__any_sync(FULLMASK, over)) {
+            // lane-best (cost, F0, g) over owned workers with a free slot
+            uint64_t bc = ~0ull, bk = ~0ull;
+    BFSIM_UNROLL_W
+            for (int j = 0; j < WPL; ++j) {
+              const int g = lane + 32 * j;
+              if (g >= G || cp[j] <= 0) continue;
+              long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+              int h = 0;
+              for (; h + 3 <= H; h += 4) {
+                const long long f0 = s_F[h * G + g], f1 = s_F[(h + 1) * G + g];
+                const long long f2 = s_F[(h + 2) * G + g], f3 = s_F[(h + 3) * G + g];
+                const long long t0 = s_T[h], t1 = s_T[h + 1], t2 = s_T[h + 2], t3 = s_T[h + 3];
+                a0 += t0 > f0 ? t0 : f0;
+                a1 += t1 > f1 ? t1 : f1;
+                a2 += t2 > f2 ? t2 : f2;
+                a3 += t3 > f3 ? t3 : f3;
+              }
+              for (; h <= H; ++h) {
+                const long long f0 = s_F[h * G + g], t0 = s_T[h];
+                a0 += t0 > f0 ? t0 : f0;
+              }
+              const uint64_t cost = static_cast<uint64_t>(a0 + a1 + a2 + a3);
+              const uint64_t k2 = (static_cast<uint64_t>(s_F[g]) << gbits) | static_cast<uint64_t>(g);
+              if (cost < bc || (cost == bc && k2 < bk)) {
+                bc = cost;
+                bk = k2;
+              }
+            }
+            const uint64_t cmin = wmin_u64(bc);
+            const uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
+            gs = static_cast<int>(kmin & gmask);
+          }
           for (int h = lane; h <= H; h += 32) {
             const long long v = s_F[h * G + gs] + s_w[h];
             s_F[h * G + gs] = v;
