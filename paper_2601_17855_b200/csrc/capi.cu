@@ -308,6 +308,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     cold(&p.o_nzb, (GB + max_len) * 4);
     cold(&p.o_abits, words * 8);
     cold(&p.o_zpre, words * 4);
+    cold(&p.o_selb, ((max_len + 31) / 32 + 2) * 4);
   }
   p.smem_per_warp = static_cast<int>((sm_off + 15) & ~15LL);
   if (p.smem_per_warp == 0) p.smem_per_warp = 16;

@@ -38,7 +38,7 @@ struct Plan {
   int64_t o_cbuf, o_misc;
   // noisy lookahead: mt19937_64 state, per-worker active lists, per-item
   // draws (hot); the step's draws, admitted-id bitmap and its word prefix (cold)
-  int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre;
+  int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre, o_selb;
   // bfio-greedy with WPL >= 16: per-worker argmin keys
   int64_t o_key;
   // completion calendar (cal != 0, large G*B): list heads [R][32], per-slot links

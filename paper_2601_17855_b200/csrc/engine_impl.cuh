@@ -387,6 +387,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* nzb = NOISY ? gat<int32_t>(ws, pl.o_nzb) : nullptr;
   unsigned long long* abits = NOISY ? gat<unsigned long long>(ws, pl.o_abits) : nullptr;
   int32_t* zpre = NOISY ? gat<int32_t>(ws, pl.o_zpre) : nullptr;
+  unsigned* selb = NOISY ? gat<unsigned>(ws, pl.o_selb) : nullptr;  // waiting ranks admitted this step
   const double sigma = sc.noise_sigma;
 
   // --- init ----------------------------------------------------------------
@@ -423,6 +424,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   if constexpr (NOISY) {
     mt_seed(s_mt, sc.seed);  // Simulation::rng_(config.seed), engine.hpp:97-98
     for (long long w = lane; w < (N + 63) / 64 + 1; w += 32) abits[w] = 0ull;
+    for (long long w = lane; w < (N + 31) / 32 + 1; w += 32) selb[w] = 0u;
   }
   __syncwarp();
 
@@ -744,9 +746,18 @@ BFSIM_UNROLL_W
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
           const long long r = got + before[t] + __popc(am[t] & lanemask_lt());
+          // values are needed for every active request's draw and for the
+          // waiting draws of requests admitted this step; the rest of the
+          // waiting draws only advance the stream
+          bool need = ((am[t] >> lane) & 1u) && r < D;
+          if (need && r >= act) {
+            const long long p = r - act;
+            need = (__ldcg(selb + (p >> 5)) >> (p & 31)) & 1u;
+          }
+          if (!__any_sync(FULLMASK, need)) continue;
           const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2v[t])), r2v[t]));
           const double nv = __dadd_rn(__dmul_rn(__dmul_rn(yv[t], mult), sigma), 0.0);
-          if (((am[t] >> lane) & 1u) && r < D) {
+          if (need) {
             long long lr = llround(nv);
             lr = lr > (1ll << 30) ? (1ll << 30) : (lr < -(1ll << 30) ? -(1ll << 30) : lr);
             nzb[r] = static_cast<int32_t>(lr);
@@ -797,7 +808,9 @@ BFSIM_UNROLL_W
     for (int q = lane; q < U; q += 32) {
       const long long id = ids[q];
       const unsigned long long below = (1ull << (id & 63)) - 1ull;
-      out[q] = zpre[(id >> 6) - aw0] + __popcll(~__ldcg(abits + (id >> 6)) & below);
+      const int rank = zpre[(id >> 6) - aw0] + __popcll(~__ldcg(abits + (id >> 6)) & below);
+      out[q] = rank;
+      atomicOr(selb + (rank >> 5), 1u << (rank & 31));
     }
     __syncwarp();
   };
@@ -1344,7 +1357,11 @@ BFSIM_UNROLL_W
         waiting_ranks(U, o_id, o_nz);
         gen_normals(act + n_wait, true);
         noisy_views();
-        for (int q = lane; q < U; q += 32) o_nz[q] = nzb[act + o_nz[q]];
+        for (int q = lane; q < U; q += 32) {
+          const int rank = o_nz[q];
+          o_nz[q] = nzb[act + rank];
+          selb[rank >> 5] = 0u;
+        }
       }
       if constexpr (HR > 0) {
         // Register-resident chain (H < HR, G <= 64, every cost < 2^31; the
@@ -1603,13 +1620,14 @@ BFSIM_UNROLL_W
   // All 32 lanes scan the finish-step array with 128-bit shared loads (four
   // independent loads in flight per lane) and append matches to per-worker
   // lists; each owner lane then retires its workers' requests in registers.
+  // (Retiring each match in place with shared atomics measured slower.)
   // TPOT terms are buffered (x, k) and evaluated off the critical path.
   auto retire = [&]() {
     const uint32_t kf = static_cast<uint32_t>(k);
     constexpr bool kWinPolicy = GREEDY && !NOISY;  // perfect/truncated finish window
     const bool win = kWinPolicy && H > 0;
     const uint32_t kh = win ? static_cast<uint32_t>(k + H) : kf;
-    const int rk = static_cast<int>(k % Hm);
+    const int rk = win ? static_cast<int>(k % Hm) : 0;
     if (win) {
 BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
