@@ -197,8 +197,10 @@ int bfsim_prepare_stream(const bfsim_sample_t* smp, int64_t n, bfsim_input_t* in
 
 /* ---- batched step engine ------------------------------------------------ */
 /* Host-pointer entry (the end-to-end path): copies inputs H2D, runs every
- * scenario, copies outputs D2H. Any sink pointer may be NULL. Returns the
- * first error over scenarios (per-scenario status in results[i].status). */
+ * scenario, copies outputs D2H. Any sink pointer may be NULL. Step sinks in
+ * page-locked host memory (cudaHostAlloc / cudaHostRegister) are written by
+ * the kernels directly (zero-copy, overlapped with the simulation). Returns
+ * the first error over scenarios (per-scenario status in results[i].status). */
 int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_scen,
                     const bfsim_input_t* inputs, int32_t n_inputs, const int32_t* class_base,
                     int64_t n_class_base, const bfsim_request_t* traces, int64_t n_trace_records,

@@ -592,7 +592,30 @@ int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_sc
     return cuda_fail(err, errlen, e, "alloc");
   bfsim_step_sink_t dsteps{};
   bool want_steps = steps && steps->clock_start && n_step_records > 0;
+  // Page-locked step sinks (cudaHostAlloc / cudaHostRegister) are written by
+  // the kernel directly over the host link: the 32-step record rows stream out
+  // while the simulation runs instead of in one copy after it.
+  bool zero_copy = false;
   if (want_steps) {
+    void* dp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    void* hp[5] = {steps->clock_start, steps->dt, steps->max_load, steps->active_count, steps->loads};
+    zero_copy = true;
+    for (int i = 0; i < 5 && zero_copy; ++i) {
+      cudaPointerAttributes a{};
+      zero_copy = hp[i] && cudaPointerGetAttributes(&a, hp[i]) == cudaSuccess &&
+                  a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+      if (zero_copy) dp[i] = a.devicePointer;
+    }
+    cudaGetLastError();  // clear a failed query on pageable memory
+    if (zero_copy) {
+      dsteps.clock_start = static_cast<double*>(dp[0]);
+      dsteps.dt = static_cast<double*>(dp[1]);
+      dsteps.max_load = static_cast<double*>(dp[2]);
+      dsteps.active_count = static_cast<int64_t*>(dp[3]);
+      dsteps.loads = static_cast<double*>(dp[4]);
+    }
+  }
+  if (want_steps && !zero_copy) {
     if ((e = ctx->st_cs.ensure(n_step_records * 8)) || (e = ctx->st_dt.ensure(n_step_records * 8)) ||
         (e = ctx->st_mx.ensure(n_step_records * 8)) || (e = ctx->st_ac.ensure(n_step_records * 8)) ||
         (e = ctx->st_ld.ensure(std::max<int64_t>(n_load_values, 1) * 8)))
@@ -627,7 +650,7 @@ int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_sc
     if (h && bytes) cudaMemcpyAsync(h, b.p, bytes, cudaMemcpyDeviceToHost, us);
   };
   down(results, ctx->results, n_scen * sizeof(bfsim_result_t));
-  if (want_steps) {
+  if (want_steps && !zero_copy) {
     down(steps->clock_start, ctx->st_cs, n_step_records * 8);
     down(steps->dt, ctx->st_dt, n_step_records * 8);
     down(steps->max_load, ctx->st_mx, n_step_records * 8);

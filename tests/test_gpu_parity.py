@@ -310,3 +310,26 @@ def test_calendar_large_slot_counts(ctx, orc):
                        emit_requests=True)
     for i in range(len(so)):
         _ovl_check(orc, br, i, br.scen[i], stream, 64)
+
+
+def test_pinned_zero_copy_sinks_match(ctx):
+    """Page-locked step sinks are written by the kernel directly (zero-copy);
+    the records equal those of the staged copy path."""
+    trs = [host.sample_instance(s, rate=1500.0, duration=1.0, s_max=64, p=0.05) for s in (1, 2)]
+    scs = np.array([abi.scenario(policy=p, workers=8, batch=16, horizon=H, input_id=i)
+                    for i in range(2) for p, H in ((abi.BFIO_GREEDY, 0), (abi.BFIO_GREEDY, 5), (abi.JSQ, 0))],
+                   abi.scenario_dtype)
+    pool = host.InputPool(trs)
+    ref = ctx.run_batch(scs, pool, emit_steps=True, emit_requests=True)
+    K = ref.res["steps_run"].astype(np.int64)
+    pb = host.PinnedBatch(ctx, scs, pool, step_capacity=np.maximum(K, 1))
+    res = pb.run()
+    np.testing.assert_array_equal(res["imb_total_i"], ref.res["imb_total_i"])
+    off = 0
+    for i in range(len(scs)):
+        k = int(K[i])
+        np.testing.assert_array_equal(pb.steps["clock_start"][off:off + k], ref.steps(i)["clock_start"])
+        np.testing.assert_array_equal(pb.steps["active_count"][off:off + k], ref.steps(i)["active_count"])
+        off += max(k, 1)
+    G = 8
+    np.testing.assert_array_equal(pb.steps["loads"][: int(K[0]) * G].reshape(-1, G), ref.steps(0)["loads"])
