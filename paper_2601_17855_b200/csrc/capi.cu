@@ -383,12 +383,17 @@ double bfsim_last_step_kernel_ms(const bfsim_ctx_t* c) {
   return static_cast<double>(ms);
 }
 
-int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, int64_t n_scen,
-                           const bfsim_input_t* inputs_host, int32_t n_inputs,
-                           const int32_t* class_base_dev, const bfsim_request_t* traces_dev,
-                           const bfsim_sample_t* streams_dev, const bfsim_step_sink_t* steps_dev,
-                           const bfsim_req_sink_t* reqs_dev, bfsim_result_t* results_dev,
-                           void* stream, char* err, size_t errlen) {
+}  // extern "C"
+
+namespace {
+// reqs_host: device-mapped page-locked mirror of the request sink; each
+// trajectory's warp copies its finished slice there (coalesced) as it ends.
+int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, int64_t n_scen,
+                          const bfsim_input_t* inputs_host, int32_t n_inputs,
+                          const int32_t* class_base_dev, const bfsim_request_t* traces_dev,
+                          const bfsim_sample_t* streams_dev, const bfsim_step_sink_t* steps_dev,
+                          const bfsim_req_sink_t* reqs_dev, const bfsim_req_sink_t* reqs_host,
+                          bfsim_result_t* results_dev, void* stream, char* err, size_t errlen) {
   if (!ctx) return fail(err, errlen, BFSIM_EINVAL, "null context");
   ctx->last_launches = 0;
   ctx->timed = false;
@@ -506,6 +511,7 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
     kp.streams = streams_dev;
     if (steps_dev) kp.steps = *steps_dev;
     if (reqs_dev) kp.reqs = *reqs_dev;
+    if (reqs_dev && reqs_host) kp.reqs_host = *reqs_host;
     kp.results = results_dev;
     kp.ws = static_cast<unsigned char*>(ctx->ws.p) + ws_off;
     kp.queue = static_cast<int32_t*>(ctx->queue.p) + gi;
@@ -525,6 +531,20 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
   ctx->timed = true;
   ctx->last_launches = launches;
   return BFSIM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, int64_t n_scen,
+                           const bfsim_input_t* inputs_host, int32_t n_inputs,
+                           const int32_t* class_base_dev, const bfsim_request_t* traces_dev,
+                           const bfsim_sample_t* streams_dev, const bfsim_step_sink_t* steps_dev,
+                           const bfsim_req_sink_t* reqs_dev, bfsim_result_t* results_dev,
+                           void* stream, char* err, size_t errlen) {
+  return run_batch_device_impl(ctx, scen_host, n_scen, inputs_host, n_inputs, class_base_dev,
+                               traces_dev, streams_dev, steps_dev, reqs_dev, nullptr, results_dev,
+                               stream, err, errlen);
 }
 
 int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_scen,
@@ -626,8 +646,32 @@ int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_sc
     dsteps.active_count = static_cast<int64_t*>(ctx->st_ac.p);
     dsteps.loads = static_cast<double*>(ctx->st_ld.p);
   }
-  bfsim_req_sink_t dreqs{};
+  bfsim_req_sink_t dreqs{}, hreqs{};
   bool want_reqs = reqs && reqs->start_step && n_req_entries > 0;
+  // Page-locked request sinks: staged in HBM (the writes are scattered by
+  // request id) and copied out per trajectory, coalesced, by its own warp
+  // when it finishes -- overlapped with the trajectories still running.
+  bool req_mirror = false;
+  if (want_reqs) {
+    void* hp[5] = {reqs->arrival_step, reqs->start_step, reqs->worker, reqs->admit_clock,
+                   reqs->finish_clock};
+    void* dp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    req_mirror = true;
+    for (int i = 0; i < 5 && req_mirror; ++i) {
+      cudaPointerAttributes a{};
+      req_mirror = hp[i] && cudaPointerGetAttributes(&a, hp[i]) == cudaSuccess &&
+                   a.type == cudaMemoryTypeHost && a.devicePointer != nullptr;
+      if (req_mirror) dp[i] = a.devicePointer;
+    }
+    cudaGetLastError();
+    if (req_mirror) {
+      hreqs.arrival_step = static_cast<int32_t*>(dp[0]);
+      hreqs.start_step = static_cast<int32_t*>(dp[1]);
+      hreqs.worker = static_cast<int32_t*>(dp[2]);
+      hreqs.admit_clock = static_cast<double*>(dp[3]);
+      hreqs.finish_clock = static_cast<double*>(dp[4]);
+    }
+  }
   if (want_reqs) {
     if ((e = ctx->rq_as.ensure(n_req_entries * 4)) || (e = ctx->rq_ss.ensure(n_req_entries * 4)) ||
         (e = ctx->rq_wk.ensure(n_req_entries * 4)) || (e = ctx->rq_ac.ensure(n_req_entries * 8)) ||
@@ -639,11 +683,11 @@ int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_sc
     dreqs.admit_clock = static_cast<double*>(ctx->rq_ac.p);
     dreqs.finish_clock = static_cast<double*>(ctx->rq_fc.p);
   }
-  int rc = bfsim_run_batch_device(
+  int rc = run_batch_device_impl(
       ctx, scen, n_scen, inputs, n_inputs, static_cast<const int32_t*>(ctx->cbase.p),
       traces ? static_cast<const bfsim_request_t*>(ctx->traces.p) : nullptr,
       streams ? static_cast<const bfsim_sample_t*>(ctx->streams.p) : nullptr,
-      want_steps ? &dsteps : nullptr, want_reqs ? &dreqs : nullptr,
+      want_steps ? &dsteps : nullptr, want_reqs ? &dreqs : nullptr, req_mirror ? &hreqs : nullptr,
       static_cast<bfsim_result_t*>(ctx->results.p), us, err, errlen);
   if (rc) return rc;
   auto down = [&](void* h, const DevBuf& b, size_t bytes) {
@@ -657,7 +701,7 @@ int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_sc
     down(steps->active_count, ctx->st_ac, n_step_records * 8);
     down(steps->loads, ctx->st_ld, n_load_values * 8);
   }
-  if (want_reqs) {
+  if (want_reqs && !req_mirror) {
     down(reqs->arrival_step, ctx->rq_as, n_req_entries * 4);
     down(reqs->start_step, ctx->rq_ss, n_req_entries * 4);
     down(reqs->worker, ctx->rq_wk, n_req_entries * 4);

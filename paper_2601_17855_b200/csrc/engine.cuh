@@ -57,6 +57,7 @@ struct KParams {
   const bfsim_sample_t* streams;
   bfsim_step_sink_t steps;  // device pointers, NULL when absent
   bfsim_req_sink_t reqs;
+  bfsim_req_sink_t reqs_host;  // optional page-locked mirror, filled per trajectory at its end
   bfsim_result_t* results;
   unsigned char* ws;
   int32_t* queue;

@@ -1888,6 +1888,20 @@ BFSIM_UNROLL_W
       P.reqs.finish_clock[ro + id] = 0.0;
     }
 
+  if (emit_reqs && P.reqs_host.start_step) {
+    // this trajectory's request slice to the page-locked host mirror,
+    // coalesced, while other trajectories are still running
+    __syncwarp();
+    __threadfence();
+    const long long nreq = N;
+    for (long long i = lane; i < nreq; i += 32) {
+      P.reqs_host.arrival_step[ro + i] = P.reqs.arrival_step[ro + i];
+      P.reqs_host.start_step[ro + i] = P.reqs.start_step[ro + i];
+      P.reqs_host.worker[ro + i] = P.reqs.worker[ro + i];
+      P.reqs_host.admit_clock[ro + i] = P.reqs.admit_clock[ro + i];
+      P.reqs_host.finish_clock[ro + i] = P.reqs.finish_clock[ro + i];
+    }
+  }
   if (emit_steps && k > scap) flags |= BFSIM_FLAG_STEP_OVERFLOW;
   if (NOISY && __any_sync(FULLMASK, ntie)) flags |= BFSIM_FLAG_NOISE_NEAR_TIE;
   if (lane == 0) {

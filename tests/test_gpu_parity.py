@@ -313,8 +313,9 @@ def test_calendar_large_slot_counts(ctx, orc):
 
 
 def test_pinned_zero_copy_sinks_match(ctx):
-    """Page-locked step sinks are written by the kernel directly (zero-copy);
-    the records equal those of the staged copy path."""
+    """Page-locked sinks: step records written by the kernel directly
+    (zero-copy), request timings copied out per trajectory; both equal the
+    staged copy path."""
     trs = [host.sample_instance(s, rate=1500.0, duration=1.0, s_max=64, p=0.05) for s in (1, 2)]
     scs = np.array([abi.scenario(policy=p, workers=8, batch=16, horizon=H, input_id=i)
                     for i in range(2) for p, H in ((abi.BFIO_GREEDY, 0), (abi.BFIO_GREEDY, 5), (abi.JSQ, 0))],
@@ -333,3 +334,9 @@ def test_pinned_zero_copy_sinks_match(ctx):
         off += max(k, 1)
     G = 8
     np.testing.assert_array_equal(pb.steps["loads"][: int(K[0]) * G].reshape(-1, G), ref.steps(0)["loads"])
+    # request timings: staged in HBM, copied out per trajectory by its warp
+    n0 = trs[0].shape[0]
+    for key in ("arrival_step", "start_step", "worker", "admit_clock", "finish_clock"):
+        np.testing.assert_array_equal(pb.reqs[key][:n0], ref.requests(0, n0)[key], err_msg=key)
+        np.testing.assert_array_equal(pb.reqs[key][-trs[1].shape[0]:], ref.requests(5, trs[1].shape[0])[key],
+                                      err_msg=key)
