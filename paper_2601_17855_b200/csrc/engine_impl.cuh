@@ -1894,13 +1894,23 @@ BFSIM_UNROLL_W
     __syncwarp();
     __threadfence();
     const long long nreq = N;
-    for (long long i = lane; i < nreq; i += 32) {
-      P.reqs_host.arrival_step[ro + i] = P.reqs.arrival_step[ro + i];
-      P.reqs_host.start_step[ro + i] = P.reqs.start_step[ro + i];
-      P.reqs_host.worker[ro + i] = P.reqs.worker[ro + i];
-      P.reqs_host.admit_clock[ro + i] = P.reqs.admit_clock[ro + i];
-      P.reqs_host.finish_clock[ro + i] = P.reqs.finish_clock[ro + i];
-    }
+    auto copy = [&](auto* dst, const auto* src) {  // 4 loads in flight per lane
+      long long i = lane;
+      for (; i + 96 < nreq; i += 128) {
+        const auto v0 = __ldcg(src + ro + i), v1 = __ldcg(src + ro + i + 32);
+        const auto v2 = __ldcg(src + ro + i + 64), v3 = __ldcg(src + ro + i + 96);
+        dst[ro + i] = v0;
+        dst[ro + i + 32] = v1;
+        dst[ro + i + 64] = v2;
+        dst[ro + i + 96] = v3;
+      }
+      for (; i < nreq; i += 32) dst[ro + i] = __ldcg(src + ro + i);
+    };
+    copy(P.reqs_host.arrival_step, P.reqs.arrival_step);
+    copy(P.reqs_host.start_step, P.reqs.start_step);
+    copy(P.reqs_host.worker, P.reqs.worker);
+    copy(P.reqs_host.admit_clock, P.reqs.admit_clock);
+    copy(P.reqs_host.finish_clock, P.reqs.finish_clock);
   }
   if (emit_steps && k > scap) flags |= BFSIM_FLAG_STEP_OVERFLOW;
   if (NOISY && __any_sync(FULLMASK, ntie)) flags |= BFSIM_FLAG_NOISE_NEAR_TIE;
