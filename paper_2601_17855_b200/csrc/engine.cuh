@@ -7,7 +7,7 @@
 
 namespace bfsim {
 
-constexpr int kWarpsPerCta = 4;  // upper bound; the planner may use fewer
+constexpr int kWarpsPerCta = 1;  // one warp (trajectory) per CTA: the planner always launches wpc = 1
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
 // Per-launch-group plan: every scenario in the group fits these maxima. Every
