@@ -28,6 +28,7 @@
  *   BFSIM_ESTREAM     5  overloaded sample stream exhausted: the host batcher
  *                        extends the stream and re-runs (never user visible from
  *                        the C++ wrapper)
+ *   BFSIM_ELIMIT      6  SearchLimitExceeded (bfio-exact, policies.hpp:174-178)
  *
  * A context is bound to one CUDA device and is not thread-safe: use one
  * context per host thread (the reference: one Simulation owns its state,
@@ -51,6 +52,7 @@ extern "C" {
 #define BFSIM_ECUDA 3
 #define BFSIM_PARTIAL 4
 #define BFSIM_ESTREAM 5
+#define BFSIM_ELIMIT 6 /* bfio-exact: SearchLimitExceeded (policies.hpp:174-178), a std::runtime_error */
 
 /* PolicyKind, policies.hpp:16 (same numbering). */
 #define BFSIM_POLICY_FCFS 0
@@ -225,6 +227,35 @@ int bfsim_run_batch_device(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, 
  * in milliseconds (CUDA events on the launching stream; 0 when unavailable). */
 int64_t bfsim_last_launch_count(const bfsim_ctx_t* ctx);
 double bfsim_last_step_kernel_ms(const bfsim_ctx_t* ctx);
+
+/* ---- batched policy operator ------------------------------------------- */
+/* One assign() call (policies.hpp:372-382): `n_waiting` previews w[0..H]
+ * (row-major doubles at preview_offset), G worker views (cap and active_count
+ * at worker_offset, future[0..H] row-major at future_offset). The pairs
+ * (waiting index, worker) land at pair_offset, 2 int32 each, in the order the
+ * reference returns them; up to 2 * min(n_waiting, sum cap) int32. */
+typedef struct bfsim_assign_call_t {
+  int32_t policy;    /* BFSIM_POLICY_*, all four including bfio-exact */
+  int32_t n_waiting;
+  int32_t workers;   /* G, 1..32 (bfio-exact: 1..16) */
+  int32_t horizon;   /* H, 0..64 (bfio-exact: 0..16) */
+  int64_t preview_offset;
+  int64_t worker_offset;
+  int64_t future_offset;
+  int64_t pair_offset;
+} bfsim_assign_call_t;
+
+/* Many independent assign() calls, one warp each on the device -- the
+ * policy-level boundary the reference's unit tests and acceptance C01/C02
+ * call (tests/policies_test.cpp, acceptance_test.cpp:117-169). Values must be
+ * integers in [0, 2^31) (exact arithmetic). Per call: n_pairs,
+ * cost (bfio-exact's cost_out, else 0) and status (BFSIM_OK or
+ * BFSIM_ELIMIT when more than search_limit full allocations exist). */
+int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64_t n_calls,
+                       const double* previews, int64_t n_previews, const double* futures,
+                       int64_t n_futures, const int32_t* caps, const int32_t* active_counts,
+                       int64_t n_workers, int64_t search_limit, int32_t* pairs, int64_t n_pairs_cap,
+                       int64_t* n_pairs, double* cost, int32_t* status, char* err, size_t errlen);
 
 /* Reducer for estimate_iir (oracle.hpp:284-312): per cell, per-trial mean
  * imbalances of FCFS and BF-IO -> mean, SEM (n-1), ratio, propagated stderr.

@@ -14,6 +14,7 @@
 
 #include "bfsim_gpu.h"
 #include "common.h"
+#include "assign.cuh"
 #include "engine.cuh"
 
 using bfsim::fail;
@@ -57,6 +58,8 @@ struct bfsim_ctx {
       rq_ss, rq_wk, rq_ac, rq_fc;
   // planner-owned buffers
   DevBuf order, ws, queue;
+  // batched assign()
+  DevBuf a_calls, a_pv, a_fut, a_caps, a_cnt, a_pairs, a_np, a_cost, a_st, a_ws;
   int64_t last_launches = 0;
   bool timed = false;
   // residency policy: 0 = as many trajectories per SM as the batch needs
@@ -356,10 +359,11 @@ void bfsim_ctx_destroy(bfsim_ctx_t* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  DevBuf* bufs[] = {&c->scen,  &c->inputs, &c->cbase, &c->traces, &c->streams, &c->results,
-                    &c->st_cs, &c->st_dt,  &c->st_mx, &c->st_ac,  &c->st_ld,   &c->rq_as,
-                    &c->rq_ss, &c->rq_wk,  &c->rq_ac, &c->rq_fc,  &c->order,   &c->ws,
-                    &c->queue};
+  DevBuf* bufs[] = {&c->scen,    &c->inputs, &c->cbase,  &c->traces, &c->streams, &c->results,
+                    &c->st_cs,   &c->st_dt,  &c->st_mx,  &c->st_ac,  &c->st_ld,   &c->rq_as,
+                    &c->rq_ss,   &c->rq_wk,  &c->rq_ac,  &c->rq_fc,  &c->order,   &c->ws,
+                    &c->queue,   &c->a_calls, &c->a_pv,  &c->a_fut,  &c->a_caps,  &c->a_cnt,
+                    &c->a_pairs, &c->a_np,   &c->a_cost, &c->a_st,   &c->a_ws};
   for (auto* b : bufs) b->release();
   for (int i = 0; i < kMaxGroups; ++i) {
     cudaStreamDestroy(c->side[i]);
@@ -717,6 +721,103 @@ int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_sc
   if (first == BFSIM_ESTREAM)
     return fail(err, errlen, BFSIM_ESTREAM, "overloaded sample stream exhausted");
   return first;
+}
+
+
+int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64_t n_calls,
+                       const double* previews, int64_t n_previews, const double* futures,
+                       int64_t n_futures, const int32_t* caps, const int32_t* active_counts,
+                       int64_t n_workers, int64_t search_limit, int32_t* pairs, int64_t n_pairs_cap,
+                       int64_t* n_pairs, double* cost, int32_t* status, char* err, size_t errlen) {
+  if (!ctx) return fail(err, errlen, BFSIM_EINVAL, "null context");
+  if (n_calls <= 0) return BFSIM_OK;
+  if (n_calls > INT32_MAX) return fail(err, errlen, BFSIM_EINVAL, "too many calls");
+  if (search_limit < 0) return fail(err, errlen, BFSIM_EINVAL, "search_limit < 0");
+  cudaSetDevice(ctx->device);
+  int n_max = 1, h_max = 0;
+  auto int_ok = [](double v) { return v >= 0.0 && v < 2147483648.0 && v == std::floor(v); };
+  for (int64_t k = 0; k < n_calls; ++k) {
+    const auto& c = calls[k];
+    if (c.policy < 0 || c.policy > 3) return fail(err, errlen, BFSIM_EINVAL, "unknown policy");
+    if (c.workers < 1 || c.workers > 32)
+      return fail(err, errlen, BFSIM_EINVAL, "GPU assign: workers must be 1..32");
+    if (c.horizon < 0 || c.horizon > 64 || c.n_waiting < 0 || c.n_waiting > 4096)
+      return fail(err, errlen, BFSIM_EINVAL, "GPU assign: horizon 0..64, n_waiting 0..4096");
+    if (c.policy == BFSIM_POLICY_BFIO_EXACT && (c.workers > 16 || c.horizon > 16 || c.n_waiting > 64))
+      return fail(err, errlen, BFSIM_EINVAL, "GPU bfio-exact: workers <= 16, horizon <= 16, n_waiting <= 64");
+    const int64_t H1 = c.horizon + 1;
+    if (c.preview_offset < 0 || c.preview_offset + c.n_waiting * H1 > n_previews ||
+        c.future_offset < 0 || c.future_offset + c.workers * H1 > n_futures || c.worker_offset < 0 ||
+        c.worker_offset + c.workers > n_workers)
+      return fail(err, errlen, BFSIM_EINVAL, "assign call: slice out of range");
+    int64_t capsum = 0;
+    for (int g = 0; g < c.workers; ++g) {
+      if (caps[c.worker_offset + g] < 0 || active_counts[c.worker_offset + g] < 0)
+        return fail(err, errlen, BFSIM_EINVAL, "assign call: negative cap or active_count");
+      capsum += caps[c.worker_offset + g];
+    }
+    const int64_t U = std::min<int64_t>(c.n_waiting, capsum);
+    if (c.pair_offset < 0 || c.pair_offset + 2 * U > n_pairs_cap)
+      return fail(err, errlen, BFSIM_EINVAL, "assign call: pair slice out of range");
+    for (int64_t j = 0; j < c.n_waiting * H1; ++j)
+      if (!int_ok(previews[c.preview_offset + j]))
+        return fail(err, errlen, BFSIM_EINVAL, "GPU assign: previews must be integers in [0, 2^31)");
+    for (int64_t j = 0; j < c.workers * H1; ++j)
+      if (!int_ok(futures[c.future_offset + j]))
+        return fail(err, errlen, BFSIM_EINVAL, "GPU assign: futures must be integers in [0, 2^31)");
+    n_max = std::max(n_max, c.n_waiting);
+    h_max = std::max(h_max, c.horizon);
+  }
+  std::vector<int64_t> pv(static_cast<size_t>(std::max<int64_t>(n_previews, 1)));
+  std::vector<int64_t> fu(static_cast<size_t>(std::max<int64_t>(n_futures, 1)));
+  for (int64_t j = 0; j < n_previews; ++j) pv[j] = static_cast<int64_t>(previews[j]);
+  for (int64_t j = 0; j < n_futures; ++j) fu[j] = static_cast<int64_t>(futures[j]);
+  bfsim::AssignParams ap{};
+  ap.n_calls = static_cast<int32_t>(n_calls);
+  ap.n_max = n_max;
+  ap.h_max = h_max;
+  auto al = [](int64_t x) { return (x + 15) & ~int64_t{15}; };
+  ap.i64_offset = al(3LL * n_max * 4);
+  ap.lane_offset = al(ap.i64_offset + (33LL * (h_max + 1)) * 8);
+  ap.lane_i64_offset = al((3LL * n_max + 33) * 4);
+  ap.lane_stride = al(ap.lane_i64_offset + (h_max + 1) * 32LL * 8);
+  ap.ws_stride = al(ap.lane_offset + 32 * ap.lane_stride);
+  ap.limit = search_limit;
+  cudaStream_t us = nullptr;
+  cudaError_t e;
+  auto up = [&](DevBuf& b, const void* h, size_t bytes) -> cudaError_t {
+    cudaError_t x = b.ensure(std::max<size_t>(bytes, 16));
+    if (x == cudaSuccess && bytes) x = cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, us);
+    return x;
+  };
+  if ((e = up(ctx->a_calls, calls, n_calls * sizeof(bfsim_assign_call_t))) ||
+      (e = up(ctx->a_pv, pv.data(), pv.size() * 8)) || (e = up(ctx->a_fut, fu.data(), fu.size() * 8)) ||
+      (e = up(ctx->a_caps, caps, n_workers * 4)) || (e = up(ctx->a_cnt, active_counts, n_workers * 4)) ||
+      (e = ctx->a_pairs.ensure(std::max<int64_t>(n_pairs_cap, 1) * 4)) ||
+      (e = ctx->a_np.ensure(n_calls * 8)) || (e = ctx->a_cost.ensure(n_calls * 8)) ||
+      (e = ctx->a_st.ensure(n_calls * 4)) || (e = ctx->a_ws.ensure(ap.ws_stride * n_calls)))
+    return cuda_fail(err, errlen, e, "assign buffers");
+  ap.calls = static_cast<const bfsim_assign_call_t*>(ctx->a_calls.p);
+  ap.previews = static_cast<const int64_t*>(ctx->a_pv.p);
+  ap.futures = static_cast<const int64_t*>(ctx->a_fut.p);
+  ap.caps = static_cast<const int32_t*>(ctx->a_caps.p);
+  ap.counts = static_cast<const int32_t*>(ctx->a_cnt.p);
+  ap.pairs = static_cast<int32_t*>(ctx->a_pairs.p);
+  ap.n_pairs = static_cast<int64_t*>(ctx->a_np.p);
+  ap.cost = static_cast<double*>(ctx->a_cost.p);
+  ap.status = static_cast<int32_t*>(ctx->a_st.p);
+  ap.ws = static_cast<unsigned char*>(ctx->a_ws.p);
+  int rc = bfsim::launch_assign(ap, us);
+  if (rc) return cuda_fail(err, errlen, static_cast<cudaError_t>(rc), "assign kernel launch");
+  ctx->last_launches = 1;
+  if (n_pairs_cap > 0) cudaMemcpyAsync(pairs, ctx->a_pairs.p, n_pairs_cap * 4, cudaMemcpyDeviceToHost, us);
+  cudaMemcpyAsync(n_pairs, ctx->a_np.p, n_calls * 8, cudaMemcpyDeviceToHost, us);
+  cudaMemcpyAsync(cost, ctx->a_cost.p, n_calls * 8, cudaMemcpyDeviceToHost, us);
+  cudaMemcpyAsync(status, ctx->a_st.p, n_calls * 4, cudaMemcpyDeviceToHost, us);
+  if ((e = cudaStreamSynchronize(us)) != cudaSuccess) return cuda_fail(err, errlen, e, "assign kernel");
+  for (int64_t k = 0; k < n_calls; ++k)
+    if (status[k] == BFSIM_ELIMIT) return fail(err, errlen, BFSIM_ELIMIT, "bfio-exact: feasible allocations exceed search limit; use bfio-greedy");
+  return BFSIM_OK;
 }
 
 }  // extern "C"

@@ -65,6 +65,8 @@ def lib():
     L.bfsim_last_step_kernel_ms.argtypes = [_vp]
     L.bfsim_last_step_kernel_ms.restype = _f64
     L.bfsim_iir_reduce.argtypes = [_vp, _vp, _i32, _i32, _vp, _vp, _sz]
+    L.bfsim_assign_batch.argtypes = [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64,
+                                     _vp, _vp, _vp, _vp, _sz]
     assert L.bfsim_abi_version() == 1
     _LIB = L
     return L
@@ -511,4 +513,63 @@ def estimate_iir(ctx: Context, batch_sizes, worker_counts, trials, steps, warmup
     out = np.zeros((len(cells), 8))
     for c, (B, G) in enumerate(cells):
         out[c] = [B, G, red[c, 0], red[c, 1], red[c, 2], red[c, 3], trials, float(np.sqrt(G) > B)]
+    return out
+
+
+class _AssignCall(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("n_waiting", C.c_int32), ("workers", C.c_int32), ("horizon", C.c_int32),
+                ("preview_offset", C.c_int64), ("worker_offset", C.c_int64), ("future_offset", C.c_int64),
+                ("pair_offset", C.c_int64)]
+
+
+def assign_batch(ctx: Context, calls, search_limit=200000):
+    """Many assign() calls (policies.hpp:372-382) in one launch, one warp each.
+
+    calls: iterable of (policy, previews [n, H+1], caps [G], active_counts [G],
+    futures [G, H+1]) with integer values. Returns, per call, (pairs, cost,
+    status): pairs as the reference returns them (list of (waiting idx,
+    worker)), cost = bfio-exact's optimum (0 for the other policies), status
+    abi.OK or abi.ELIMIT (SearchLimitExceeded)."""
+    L, err = lib(), _err()
+    calls = list(calls)
+    n = len(calls)
+    arr = (_AssignCall * max(n, 1))()
+    pv_parts, fu_parts, caps_parts, cnt_parts = [], [], [], []
+    pvo = fuo = wo = po = 0
+    for k, (pol, pv, caps, cnt, fut) in enumerate(calls):
+        caps = np.asarray(caps, np.int32).reshape(-1)
+        G = caps.shape[0]
+        fut = np.asarray(fut, np.float64).reshape(G, -1)
+        H = fut.shape[1] - 1
+        pv = np.asarray(pv, np.float64).reshape(-1, H + 1)
+        nw = pv.shape[0]
+        U = min(nw, int(caps.clip(min=0).sum()))
+        arr[k] = _AssignCall(int(pol), nw, G, H, pvo, wo, fuo, po)
+        pv_parts.append(pv.reshape(-1))
+        fu_parts.append(fut.reshape(-1))
+        caps_parts.append(caps)
+        cnt_parts.append(np.asarray(cnt, np.int32).reshape(-1))
+        pvo += pv.size
+        fuo += fut.size
+        wo += G
+        po += 2 * U
+    pv_all = np.ascontiguousarray(np.concatenate(pv_parts) if pv_parts else np.zeros(1))
+    fu_all = np.ascontiguousarray(np.concatenate(fu_parts) if fu_parts else np.zeros(1))
+    caps_all = np.ascontiguousarray(np.concatenate(caps_parts) if caps_parts else np.zeros(1, np.int32))
+    cnt_all = np.ascontiguousarray(np.concatenate(cnt_parts) if cnt_parts else np.zeros(1, np.int32))
+    pairs = np.zeros(max(po, 1), np.int32)
+    npairs = np.zeros(max(n, 1), np.int64)
+    cost = np.zeros(max(n, 1))
+    status = np.zeros(max(n, 1), np.int32)
+    rc = L.bfsim_assign_batch(ctx.h, C.byref(arr), n, abi.ptr(pv_all), pvo, abi.ptr(fu_all), fuo, abi.ptr(caps_all),
+                              abi.ptr(cnt_all), wo, int(search_limit), abi.ptr(pairs), po, abi.ptr(npairs),
+                              abi.ptr(cost), abi.ptr(status), err, 1024)
+    if rc not in (abi.OK, abi.ELIMIT):
+        _raise(rc, err)
+    out = []
+    for k in range(n):
+        o = int(arr[k].pair_offset)
+        m = int(npairs[k])
+        pr = [(int(pairs[o + 2 * j]), int(pairs[o + 2 * j + 1])) for j in range(m)]
+        out.append((pr, float(cost[k]), int(status[k])))
     return out
