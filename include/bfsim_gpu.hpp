@@ -476,5 +476,60 @@ inline IirEstimate estimate_iir(Context& ctx, const std::vector<int>& batch_size
   return est;
 }
 
+// One policy call as the reference makes it: assign(policy, waiting,
+// workers, H, search_limit), policies.hpp:372-382.
+struct AssignCall {
+  PolicyKind policy;
+  const std::vector<RequestPreview>* waiting;
+  const std::vector<WorkerView>* workers;
+  int H;
+};
+
+// Many independent assign() calls in one launch (one warp each on the
+// device). Returns the reference's Allocations; throws what assign() would
+// (SearchLimitExceeded for bfio-exact beyond search_limit, invalid_argument
+// for values the GPU path cannot take exactly).
+inline std::vector<Allocation> assign_batch(Context& ctx, const std::vector<AssignCall>& calls,
+                                            long search_limit = 200000,
+                                            std::vector<double>* exact_costs = nullptr) {
+  std::vector<bfsim_assign_call_t> c(calls.size());
+  std::vector<double> pv, fu;
+  std::vector<int32_t> caps, cnt;
+  int64_t pairs = 0;
+  for (size_t k = 0; k < calls.size(); ++k) {
+    const auto& a = calls[k];
+    const int G = static_cast<int>(a.workers->size());
+    long capsum = 0;
+    c[k] = bfsim_assign_call_t{static_cast<int32_t>(a.policy), static_cast<int32_t>(a.waiting->size()), G, a.H,
+                               static_cast<int64_t>(pv.size()), static_cast<int64_t>(caps.size()),
+                               static_cast<int64_t>(fu.size()), pairs};
+    for (const auto& r : *a.waiting) pv.insert(pv.end(), r.w.begin(), r.w.begin() + a.H + 1);
+    for (const auto& w : *a.workers) {
+      caps.push_back(w.cap);
+      cnt.push_back(w.active_count);
+      fu.insert(fu.end(), w.future.begin(), w.future.begin() + a.H + 1);
+      capsum += w.cap > 0 ? w.cap : 0;
+    }
+    pairs += 2 * std::min<long>(static_cast<long>(a.waiting->size()), capsum);
+  }
+  std::vector<int32_t> out(static_cast<size_t>(std::max<int64_t>(pairs, 1)));
+  std::vector<int64_t> np(calls.size());
+  std::vector<double> cost(calls.size());
+  std::vector<int32_t> st(calls.size());
+  char err[1024] = {0};
+  int rc = bfsim_assign_batch(ctx.get(), c.data(), static_cast<int64_t>(c.size()), pv.data(),
+                              static_cast<int64_t>(pv.size()), fu.data(), static_cast<int64_t>(fu.size()),
+                              caps.data(), cnt.data(), static_cast<int64_t>(caps.size()), search_limit,
+                              out.data(), pairs, np.data(), cost.data(), st.data(), err, sizeof err);
+  if (rc == BFSIM_ELIMIT) throw SearchLimitExceeded(search_limit);
+  check(rc, err);
+  std::vector<Allocation> res(calls.size());
+  for (size_t k = 0; k < calls.size(); ++k)
+    for (int64_t j = 0; j < np[k]; ++j)
+      res[k].assignments.emplace_back(out[c[k].pair_offset + 2 * j], out[c[k].pair_offset + 2 * j + 1]);
+  if (exact_costs) *exact_costs = cost;
+  return res;
+}
+
 }  // namespace gpu
 }  // namespace bfsim

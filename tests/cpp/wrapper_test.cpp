@@ -229,6 +229,51 @@ int main() {
     ok = ok && a.str() == b.str();
     report("write_step_csv / write_summary / write_iir_csv byte-identical (C1, noisy H=20)", ok);
   }
+  {  // the policy operator: gpu::assign_batch == assign() on random steps,
+     // every policy (policies_test.cpp random_step shapes, :27-55)
+    std::mt19937_64 rng(4242);
+    std::vector<std::vector<RequestPreview>> ws;
+    std::vector<std::vector<WorkerView>> vs;
+    std::vector<gpu::AssignCall> calls;
+    std::vector<int> hs;
+    for (int t = 0; t < 2000; ++t) {
+      int H = static_cast<int>(rng() % 3), G = 1 + static_cast<int>(rng() % 3), n = static_cast<int>(rng() % 7);
+      std::vector<WorkerView> v(static_cast<size_t>(G));
+      for (auto& w : v) {
+        w.cap = static_cast<int>(rng() % 4);
+        w.active_count = static_cast<int>(rng() % 3);
+        for (int h = 0; h <= H; ++h) w.future.push_back(static_cast<double>(rng() % 20));
+      }
+      std::vector<RequestPreview> q(static_cast<size_t>(n));
+      for (auto& r : q)
+        for (int h = 0; h <= H; ++h) r.w.push_back(static_cast<double>(rng() % 10));
+      ws.push_back(std::move(q));
+      vs.push_back(std::move(v));
+      hs.push_back(H);
+    }
+    for (size_t t = 0; t < ws.size(); ++t)
+      calls.push_back({std::vector<PolicyKind>{PolicyKind::Fcfs, PolicyKind::Jsq, PolicyKind::BfioExact,
+                                               PolicyKind::BfioGreedy}[t % 4],
+                       &ws[t], &vs[t], hs[t]});
+    auto got = gpu::assign_batch(ctx, calls);
+    bool ok = got.size() == calls.size();
+    for (size_t t = 0; ok && t < calls.size(); ++t)
+      ok = got[t].assignments == assign(calls[t].policy, ws[t], vs[t], hs[t], 200000).assignments;
+    bool threw = false;
+    std::vector<WorkerView> v4(4);
+    for (auto& w : v4) {
+      w.cap = 4;
+      w.future = {0.0};
+    }
+    std::vector<RequestPreview> q12(12);
+    for (auto& r : q12) r.w = {1.0};
+    try {
+      gpu::assign_batch(ctx, {{PolicyKind::BfioExact, &q12, &v4, 0}}, 100);
+    } catch (const SearchLimitExceeded&) {
+      threw = true;
+    }
+    report("gpu::assign_batch == assign (2000 random steps, 4 policies) + SearchLimitExceeded", ok && threw);
+  }
   {  // acceptance_test.cpp:178-180 (C04) through the GPU path
     OverloadedSpec spec;
     spec.prefill = PrefillDistribution::uniform(64);
