@@ -1426,20 +1426,19 @@ BFSIM_UNROLL_W
           const uint64_t km = wmin_u64(best);
           const int gs = static_cast<int>(km & gmask);
           const int own = gs & 31, jj = gs >> 5;
-          // the chosen row gains w_h (broadcast from lane h); lane h then
-          // raises M_h with the row's new value (broadcast from the owner)
-#pragma unroll
-          for (int h = 0; h < HR; ++h) {
-            const int32_t w = __shfl_sync(FULLMASK, wl, h);
-#pragma unroll
-            for (int j = 0; j < WPL; ++j) Fr[j][h] += (lane == own && j == jj) ? w : 0;
-            const int32_t nv = __shfl_sync(FULLMASK, (WPL > 1 && jj) ? Fr[WPL - 1][h] : Fr[0][h], own);
-            Ml = (lane == h && nv > Ml) ? nv : Ml;
-          }
+          // the owner adds w_h to the chosen row (recomputing w_h, no per-item
+          // array) and publishes the row; lane h then raises M_h with it
+          int32_t* s_row = reinterpret_cast<int32_t*>(s_M);
           if (lane == own) {
 #pragma unroll
             for (int j = 0; j < WPL; ++j)
               if (j == jj) {
+#pragma unroll
+                for (int h = 0; h < HR; ++h) {
+                  const int32_t dh = d32 * h;
+                  Fr[j][h] += h < limH ? c + (dh < sat ? dh : sat) : 0;
+                  s_row[h] = Fr[j][h];
+                }
                 cp[j] -= 1;
                 A[j] += c + ak;
                 s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
@@ -1451,6 +1450,9 @@ BFSIM_UNROLL_W
                 }
               }
           }
+          __syncwarp();
+          if (lane < HR) Ml = s_row[lane] > Ml ? s_row[lane] : Ml;
+          __syncwarp();
         }
         __syncwarp();
       } else {
