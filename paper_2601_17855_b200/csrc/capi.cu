@@ -156,10 +156,10 @@ int bits_for(int64_t x) {  // bits to hold values 0..x (the kernel's bits_for)
 }
 
 // Width of the register-resident lookahead chain (engine_impl.cuh, HR):
-// bfio-greedy with 0 < H < 24 on G <= 64 workers whose per-worker loads fit
+// bfio-greedy with 0 < H < 24 on G <= 128 workers whose per-worker loads fit
 // 31 bits with the worker index and whose horizon costs fit 31 bits.
 int reg_chain_width(const bfsim_scenario_t& s, const bfsim_input_t& in) {
-  if (s.policy != BFSIM_POLICY_BFIO_GREEDY || s.horizon <= 0 || s.horizon >= 24 || s.workers > 64)
+  if (s.policy != BFSIM_POLICY_BFIO_GREEDY || s.horizon <= 0 || s.horizon >= 24 || s.workers > 128)
     return 0;
   const int64_t d = static_cast<int64_t>(s.drift);
   const int64_t lbound = static_cast<int64_t>(s.batch) * (in.s_max + d * (in.max_decode - 1));

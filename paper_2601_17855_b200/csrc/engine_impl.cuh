@@ -303,7 +303,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   constexpr bool OVL = MODE == BFSIM_MODE_OVERLOADED;
   constexpr bool GREEDY = POL == BFSIM_POLICY_BFIO_GREEDY;
   static_assert(!NOISY || (GREEDY && !OVL), "noisy lookahead: Poisson bfio-greedy only");
-  static_assert(HR == 0 || (GREEDY && WPL <= 2), "register lookahead chain: bfio-greedy, G <= 64");
+  static_assert(HR == 0 || (GREEDY && WPL <= 4), "register lookahead chain: bfio-greedy, G <= 128");
   constexpr bool JSQ = POL == BFSIM_POLICY_JSQ;
   const Plan& pl = P.plan;
   const int lane = threadIdx.x & 31;
@@ -1991,6 +1991,8 @@ int launch_w(int wpl, int hr, const KParams& kp, int grid, int wpc, cudaStream_t
     if (hr == 8 && wpl == 2) return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 8>(kp, grid, wpc, s, occ);
     if (hr == 24 && wpl == 1) return launch_t<MODE, POL, 1, SMALLC, SM, NOISY, 24>(kp, grid, wpc, s, occ);
     if (hr == 24 && wpl == 2) return launch_t<MODE, POL, 2, SMALLC, SM, NOISY, 24>(kp, grid, wpc, s, occ);
+    if (hr == 8 && wpl == 4) return launch_t<MODE, POL, 4, SMALLC, SM, NOISY, 8>(kp, grid, wpc, s, occ);
+    if (hr == 24 && wpl == 4) return launch_t<MODE, POL, 4, SMALLC, SM, NOISY, 24>(kp, grid, wpc, s, occ);
   }
   if (hr != 0) return static_cast<int>(cudaErrorInvalidValue);
   switch (wpl) {
