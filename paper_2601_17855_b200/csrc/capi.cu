@@ -225,7 +225,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   };
   // completion calendar instead of the per-step finish-step scan once the
   // slot arrays outgrow shared memory (the scan's per-worker lists go away)
-  p.cal = GB > 4096 ? 1 : 0;
+  p.cal = GB > 4096 ? 1 : 2;
   p.noisy = g.noisy;
   p.cbuf = static_cast<int>(std::min<int64_t>(GB + 512, 1 << 24));
   // Hot and small first (first fit: an array that does not fit spills to
@@ -257,7 +257,10 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
   }
-  if (!p.cal) items.push_back({&p.o_rlist, GB * 2});
+  if (p.cal == 2) {  // the 32-bucket completion wheel lives in shared memory
+    items.push_back({&p.o_calh, 32LL * std::min(G, 32) * 4});
+    items.push_back({&p.o_calnx, GB * 2});
+  }
   const size_t n_hot = items.size();  // the residency planner tries to keep these in shared memory
   items.push_back({&p.o_id, GB * 4});
   items.push_back({&p.o_x, GB * 4});
@@ -301,7 +304,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   };
   cold(&p.o_ring, R * 8LL);
   cold(&p.o_cbuf, static_cast<int64_t>(p.cbuf) * 8);
-  if (p.cal) {
+  if (p.cal == 1) {
     cold(&p.o_calh, static_cast<int64_t>(R) * 32 * 4);
     cold(&p.o_calnx, GB * 4);
   }

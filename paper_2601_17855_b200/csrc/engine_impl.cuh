@@ -375,9 +375,15 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   uint64_t* s_key = (GREEDY && WPL >= 16) ? at<SM, uint64_t>(sm, ws, pl.o_key) : nullptr;
   // Completion calendar (large G*B): bucket f mod R holds, per owner lane
   // (g mod 32), a linked list of the slots finishing at step f.
-  const bool cal = pl.cal != 0;
-  int32_t* calh = cal ? gat<int32_t>(ws, pl.o_calh) : nullptr;
-  int32_t* calnx = cal ? gat<int32_t>(ws, pl.o_calnx) : nullptr;
+  // cal 1 (G*B > 4096): bucket f mod R exactly, in the global workspace.
+  // cal 2 (small G*B): a 32-bucket wheel in shared memory, bucket f mod 32;
+  // an entry is retired when its bucket comes round at its finish step.
+  const int cal = pl.cal;
+  constexpr int kWheel = 32;
+  const int LS = G < 32 ? G : 32;  // lanes that own workers (wheel row stride)
+  int32_t* calh = cal == 1 ? gat<int32_t>(ws, pl.o_calh) : (cal == 2 ? at<SM, int32_t>(sm, ws, pl.o_calh) : nullptr);
+  int32_t* calnx = cal == 1 ? gat<int32_t>(ws, pl.o_calnx) : nullptr;
+  uint16_t* wnx = cal == 2 ? at<SM, uint16_t>(sm, ws, pl.o_calnx) : nullptr;
   // Noisy lookahead (NOISY): engine state, per-worker active lists in
   // insertion order (interleaved [pos * G + g]), per-item draws, the step's
   // draws and the admitted-id bitmap that gives waiting ranks.
@@ -416,8 +422,10 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     wset.init(bm, bm + 64, S);
     pset.init(pbm, pbm + 64, S);
   }
-  if (cal)
+  if (cal == 1)
     for (int i = lane; i < pl.R * 32; i += 32) calh[i] = -1;
+  if (cal == 2)
+    for (int i = lane; i < kWheel * LS; i += 32) calh[i] = -1;
   int mt_i = kMtN;       // next engine word in the current block (always even)
   long long aw0 = 0;     // first bitmap word holding a waiting (revealed, unadmitted) id
   bool ntie = false;     // a draw landed next to an lround tie (BFSIM_FLAG_NOISE_NEAR_TIE)
@@ -696,9 +704,13 @@ BFSIM_UNROLL_W
     s_a[slot] = static_cast<int32_t>(s - d * k);
     s_x[slot] = static_cast<int32_t>(k);
     s_id[slot] = static_cast<int32_t>(id);
-    if (cal) {
+    if (cal == 1) {
       const int b = static_cast<int>((k + o - 1) & Rm);
       calnx[slot] = atomicExch(&calh[b * 32 + (g & 31)], slot);
+    } else if (cal == 2) {
+      const int b = static_cast<int>((k + o - 1) & (kWheel - 1));
+      const int old = atomicExch(&calh[b * LS + (g & 31)], slot);
+      wnx[slot] = static_cast<uint16_t>(old < 0 ? 0xFFFF : old);
     }
     if (emit_reqs) {
       P.reqs.start_step[ro + id] = static_cast<int32_t>(k);
@@ -1651,30 +1663,54 @@ BFSIM_UNROLL_W
       // Calendar: each lane walks its own lists (it owns every worker on
       // them, so worker state needs no atomics). Window entries first: the
       // slots finishing at k + H stay listed.
+      const bool wheel = cal == 2;
+      auto head_of = [&](long long kk) -> int32_t* {
+        return wheel ? (lane < LS ? &calh[static_cast<int>(kk & (kWheel - 1)) * LS + lane] : nullptr)
+                     : &calh[static_cast<int>(kk & Rm) * 32 + lane];
+      };
+      auto next_of = [&](int slot) -> int {
+        if (wheel) {
+          const uint16_t v = wnx[slot];
+          return v == 0xFFFF ? -1 : static_cast<int>(v);
+        }
+        return calnx[slot];
+      };
       if (win) {
-        for (int s = calh[static_cast<int>((k + H) & Rm) * 32 + lane]; s >= 0; s = calnx[s]) {
+        int32_t* hp = head_of(k + H);
+        for (int s = hp ? *hp : -1; s >= 0; s = next_of(s)) {
+          if (wheel && s_f[s] != kh) continue;
           const int g = slot_worker(s);
           s_Wc[rk * G + g] += 1;
           s_Wa[rk * G + g] += s_a[s];
         }
       }
-      const int b = static_cast<int>(k & Rm);
-      int s = calh[b * 32 + lane];
-      calh[b * 32 + lane] = -1;
+      int32_t* hb = head_of(k);
+      int s = hb ? *hb : -1;
+      if (!wheel) *hb = -1;
+      int prev = -1;
       int rc[WPL];
 BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) rc[j] = 0;
       int nd = 0;
       while (__any_sync(FULLMASK, s >= 0)) {
-        const bool live = s >= 0;
+        const int nx = s >= 0 ? next_of(s) : -1;
+        const bool live = s >= 0 && (!wheel || s_f[s] == static_cast<uint32_t>(k));
+        if (wheel && s >= 0 && !live) prev = s;  // a later lap: stays listed
         const unsigned am = __ballot_sync(FULLMASK, live);
-        const int leader = __ffs(am) - 1;
         int base = 0;
-        if (lane == leader) base = atomicAdd(&s_misc[0], __popc(am));
-        base = __shfl_sync(FULLMASK, base, leader);
+        if (am) {
+          const int leader = __ffs(am) - 1;
+          if (lane == leader) base = atomicAdd(&s_misc[0], __popc(am));
+          base = __shfl_sync(FULLMASK, base, leader);
+        }
+        if (!live) s = nx;
         if (live) {
           const int slot = s;
-          s = calnx[slot];
+          s = nx;
+          if (wheel) {  // unlink
+            if (prev < 0) *hb = nx;
+            else wnx[prev] = static_cast<uint16_t>(nx < 0 ? 0xFFFF : nx);
+          }
           const int g = slot_worker(slot);
           const int i = slot - g * B;
           const int jj = g >> 5;
