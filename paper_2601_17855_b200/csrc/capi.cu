@@ -223,8 +223,8 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     int64_t* code;
     int64_t bytes;
   };
-  // completion calendar instead of the per-step finish-step scan once the
-  // slot arrays outgrow shared memory (the scan's per-worker lists go away)
+  // completion calendar: a 32-bucket wheel in shared memory for small G*B,
+  // exact finish-step buckets in the workspace once the slots outgrow it
   p.cal = GB > 4096 ? 1 : 2;
   p.noisy = g.noisy;
   p.cbuf = static_cast<int>(std::min<int64_t>(GB + 512, 1 << 24));

@@ -353,7 +353,6 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   // per-class record {front, back, picks this step, deque base} + chain start
   int4* c_rec = at<SM, int4>(sm, ws, pl.o_cls);
   int32_t* c_cs = reinterpret_cast<int32_t*>(c_rec + (pl.S + 2));
-  uint16_t* s_rlist = at<SM, uint16_t>(sm, ws, pl.o_rlist);
   int2* deq = gat<int2>(ws, pl.o_deq);
   int2* stage = at<SM, int2>(sm, ws, pl.o_stage);  // prefetched (id|s, o) records
   int32_t* p_cl = at<SM, int32_t>(sm, ws, pl.o_pcl);
@@ -1631,11 +1630,11 @@ BFSIM_UNROLL_W
   };
 
   // ---- retire requests finishing at step k (+ window entry at k + H) ----
-  // All 32 lanes scan the finish-step array with 128-bit shared loads (four
-  // independent loads in flight per lane) and append matches to per-worker
-  // lists; each owner lane then retires its workers' requests in registers.
-  // (Retiring each match in place with shared atomics measured slower.)
-  // TPOT terms are buffered (x, k) and evaluated off the critical path.
+  // A completion calendar (a 32-bucket wheel in shared memory, or exact
+  // buckets in the workspace for large G*B) holds, per owner lane, the slots
+  // finishing in each bucket: a step touches only its completions (and, on
+  // the wheel, entries a lap away), not every slot. Owner lanes retire in
+  // registers; TPOT terms are buffered (x, k) and evaluated off the chain.
   auto retire = [&]() {
     const uint32_t kf = static_cast<uint32_t>(k);
     constexpr bool kWinPolicy = GREEDY && !NOISY;  // perfect/truncated finish window
@@ -1659,7 +1658,7 @@ BFSIM_UNROLL_W
       g += ((g + 1) * B <= slot) ? 1 : 0;
       return g;
     };
-    if (cal) {
+    {
       // Calendar: each lane walks its own lists (it owns every worker on
       // them, so worker state needs no atomics). Window entries first: the
       // slots finishing at k + H stay listed.
@@ -1752,89 +1751,7 @@ BFSIM_UNROLL_W
       const long long ndw = static_cast<long long>(__reduce_add_sync(FULLMASK, static_cast<unsigned>(nd)));
       done += ndw;
       act -= ndw;
-      return;
     }
-    const int nslot4 = (G * B + 3) >> 2;
-    const uint4* f4 = reinterpret_cast<const uint4*>(s_f);
-    auto match = [&](uint4 v, uint32_t key) -> uint32_t {
-      return (v.x == key ? 1u : 0u) | (v.y == key ? 2u : 0u) | (v.z == key ? 4u : 0u) |
-             (v.w == key ? 8u : 0u);
-    };
-    auto hit = [&](int q, uint32_t m, uint32_t me) {
-      while (m | me) {
-        const int c = __ffs(m | me) - 1;
-        const bool fin = (m >> c) & 1u;
-        m &= ~(1u << c);
-        me &= ~(1u << c);
-        const int slot = 4 * q + c;
-        const int g = slot_worker(slot);
-        if (fin) {
-          const int pos = atomicAdd(&s_rn[g], 1);
-          s_rlist[g * B + pos] = static_cast<uint16_t>(slot - g * B);
-        } else {  // enters the lookahead window [k+1, k+H]
-          atomicAdd(&s_Wc[rk * G + g], 1);
-          atomicAdd(reinterpret_cast<unsigned long long*>(&s_Wa[rk * G + g]),
-                    static_cast<unsigned long long>(static_cast<long long>(s_a[slot])));
-        }
-      }
-    };
-    int q = lane;
-    for (; q + 96 < nslot4; q += 128) {
-      const uint4 v0 = f4[q], v1 = f4[q + 32], v2 = f4[q + 64], v3 = f4[q + 96];
-      const uint32_t m0 = match(v0, kf), m1 = match(v1, kf), m2 = match(v2, kf), m3 = match(v3, kf);
-      uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-      if (win) {
-        e0 = match(v0, kh);
-        e1 = match(v1, kh);
-        e2 = match(v2, kh);
-        e3 = match(v3, kh);
-      }
-      if (m0 | m1 | m2 | m3 | e0 | e1 | e2 | e3) {
-        hit(q, m0, e0);
-        hit(q + 32, m1, e1);
-        hit(q + 64, m2, e2);
-        hit(q + 96, m3, e3);
-      }
-    }
-    for (; q < nslot4; q += 32) {
-      const uint4 v = f4[q];
-      hit(q, match(v, kf), win ? match(v, kh) : 0u);
-    }
-    __syncwarp();
-    int nd = 0;
-BFSIM_UNROLL_W
-    for (int j = 0; j < WPL; ++j) {
-      const int g = lane + 32 * j;
-      if (g >= G) continue;
-      const int nr = s_rn[g];
-      if (nr == 0) continue;
-      s_rn[g] = 0;
-      int cap = B - n[j];
-      const int cb0 = atomicAdd(&s_misc[0], nr);
-      for (int e = 0; e < nr; ++e) {
-        const int i = s_rlist[g * B + e];
-        const int slot = g * B + i;
-        A[j] -= s_a[slot];
-        s_stk[g * B + cap] = static_cast<uint16_t>(i);
-        ++cap;
-        s_f[slot] = kEmpty;
-        cbuf[cb0 + e] = make_int2(s_x[slot], static_cast<int>(k));
-        if (emit_reqs) P.reqs.finish_clock[ro + s_id[slot]] = clock;
-      }
-      if constexpr (NOISY) {  // erase_if keeps insertion order (engine.hpp:118-120)
-        int w = 0;
-        for (int p = 0; p < n[j]; ++p) {
-          const uint16_t i = s_lst[p * G + g];
-          if (s_f[g * B + i] != kEmpty) s_lst[(w++) * G + g] = i;
-        }
-      }
-      n[j] -= nr;
-      nd += nr;
-      s_cap[g] = cap;
-    }
-    const long long ndw = static_cast<long long>(__reduce_add_sync(FULLMASK, static_cast<unsigned>(nd)));
-    done += ndw;
-    act -= ndw;
   };
 
   // --- step loop -----------------------------------------------------------
