@@ -351,9 +351,16 @@ def run_ours(args):
     from paper_2601_17855_b200 import abi, host, parallel
 
     rank, local, world = env_rank()
+    # one process per GPU; the modulo and the backend override only matter
+    # for exercising the multi-rank path on a single-GPU box (gloo)
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BFSIM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
