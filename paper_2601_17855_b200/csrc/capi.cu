@@ -63,9 +63,7 @@ struct bfsim_ctx {
   DevBuf a_calls, a_pv, a_fut, a_caps, a_cnt, a_pairs, a_np, a_cost, a_st, a_ws;
   int64_t last_launches = 0;
   bool timed = false;
-  // residency policy: 0 = as many trajectories per SM as the batch needs
-  // (measured best on C3); 1 = cap it so the hot arrays stay in shared memory
-  int fit_hot = 0;
+
 };
 
 namespace {
@@ -223,7 +221,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     int64_t* code;
     int64_t bytes;
   };
-  // completion calendar: a 32-bucket wheel in shared memory for small G*B,
+  // completion calendar: a 64-bucket wheel in shared memory for small G*B,
   // exact finish-step buckets in the workspace once the slots outgrow it
   p.cal = GB > 4096 ? 1 : 2;
   p.noisy = g.noisy;
@@ -235,9 +233,13 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   std::vector<Item> items = {
       {&p.o_rdt, 32 * 8}, {&p.o_rcs, 32 * 8}, {&p.o_rmx, 32 * 4}, {&p.o_rac, 32 * 4},
       {&p.o_misc, 16},    {&p.o_capb, G * 4LL}, {&p.o_asum, G * 8LL}, {&p.o_cap, G * 4LL},
-      {&p.o_rn, G * 4LL}, {&p.o_lvT, lvl * 4}, {&p.o_lvV, lvl * 4},  {&p.o_lvK, lvl * 4},
-      {&p.o_lvM, lvl * wpl * 4},
   };
+  if (!greedy) {  // level tables of the FIFO policies
+    items.push_back({&p.o_lvT, lvl * 4});
+    items.push_back({&p.o_lvV, lvl * 4});
+    items.push_back({&p.o_lvK, lvl * 4});
+    items.push_back({&p.o_lvM, lvl * wpl * 4});
+  }
   if (greedy || ovl) {
     items.push_back({&p.o_cls, 5LL * (S + 2) * 4});  // int4 records + int32 starts
     items.push_back({&p.o_bm, bm_words * 8});
@@ -257,8 +259,8 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
   }
-  if (p.cal == 2) {  // the 32-bucket completion wheel lives in shared memory
-    items.push_back({&p.o_calh, 32LL * std::min(G, 32) * 4});
+  if (p.cal == 2) {  // the 64-bucket completion wheel lives in shared memory
+    items.push_back({&p.o_calh, 64LL * std::min(G, 32) * 4});
     items.push_back({&p.o_calnx, GB * 2});
   }
   const size_t n_hot = items.size();  // the residency planner tries to keep these in shared memory
@@ -455,17 +457,11 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
     // to hold every group of the batch at once (the groups run concurrently
     // and the warps are latency-bound); what does not fit spills to the
     // per-warp global workspace (generic-addressing kernel variant)
-    // Residency: enough trajectories per SM for the whole batch, but never
-    // so many that the per-step working set (the planner's hot arrays)
-    // leaves shared memory -- a latency-bound warp that misses to L2 on every
-    // slot access is slower than a second wave of warps that do not.
+    // Residency: enough trajectories per SM for the whole batch (measured
+    // better on C3 than capping residency to keep the hot arrays in shared
+    // memory: more warps in flight beat fewer, faster ones).
     int64_t per_sm = (n_scen + ctx->sm_count - 1) / ctx->sm_count;
     per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, 16));
-    if (ctx->fit_hot) {
-      make_plan(g, scen_host, inputs_host, 1 << 30);  // dry run: size of the hot set
-      const int64_t fit = (228 * 1024) / (g.hot_bytes + 2048 + 1024);
-      per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, fit));
-    }
     int budget = static_cast<int>(std::min<int64_t>(ctx->smem_optin - 1024,
                                                     (228 * 1024) / per_sm - 2048));
     budget = std::max(budget, 8 * 1024);

@@ -22,7 +22,7 @@ struct Plan {
   int all_smem;  // every array placed in shared memory (32-bit addressing variant)
   int64_t ws_stride;
   // slots
-  int64_t o_f, o_a, o_x, o_id, o_stk, o_capb, o_asum, o_cap, o_rn, o_rlist;
+  int64_t o_f, o_a, o_x, o_id, o_stk, o_capb, o_asum, o_cap;
   // per-step accounting ring (32 steps) and clock ring
   int64_t o_rl, o_rdt, o_rcs, o_rmx, o_rac, o_ring;
   // FCFS/JSQ level tables

@@ -342,7 +342,6 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* s_capb = at<SM, int32_t>(sm, ws, pl.o_capb);
   unsigned long long* s_asum = at<SM, unsigned long long>(sm, ws, pl.o_asum);
   int32_t* s_cap = at<SM, int32_t>(sm, ws, pl.o_cap);
-  int32_t* s_rn = at<SM, int32_t>(sm, ws, pl.o_rn);
   uint32_t* r_l = at<SM, uint32_t>(sm, ws, pl.o_rl);
   double* r_dt = at<SM, double>(sm, ws, pl.o_rdt);
   double* r_cs = at<SM, double>(sm, ws, pl.o_rcs);
@@ -375,10 +374,10 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   // Completion calendar (large G*B): bucket f mod R holds, per owner lane
   // (g mod 32), a linked list of the slots finishing at step f.
   // cal 1 (G*B > 4096): bucket f mod R exactly, in the global workspace.
-  // cal 2 (small G*B): a 32-bucket wheel in shared memory, bucket f mod 32;
+  // cal 2 (small G*B): a 64-bucket wheel in shared memory, bucket f mod 64;
   // an entry is retired when its bucket comes round at its finish step.
   const int cal = pl.cal;
-  constexpr int kWheel = 32;
+  constexpr int kWheel = 64;
   const int LS = G < 32 ? G : 32;  // lanes that own workers (wheel row stride)
   int32_t* calh = cal == 1 ? gat<int32_t>(ws, pl.o_calh) : (cal == 2 ? at<SM, int32_t>(sm, ws, pl.o_calh) : nullptr);
   int32_t* calnx = cal == 1 ? gat<int32_t>(ws, pl.o_calnx) : nullptr;
@@ -402,7 +401,6 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   }
   for (int i = lane; i < G; i += 32) {
     s_cap[i] = B;
-    s_rn[i] = 0;
     s_asum[i] = 0;
   }
   if (lane == 0) s_misc[0] = 0;
@@ -1645,7 +1643,7 @@ BFSIM_UNROLL_W
   };
 
   // ---- retire requests finishing at step k (+ window entry at k + H) ----
-  // A completion calendar (a 32-bucket wheel in shared memory, or exact
+  // A completion calendar (a 64-bucket wheel in shared memory, or exact
   // buckets in the workspace for large G*B) holds, per owner lane, the slots
   // finishing in each bucket: a step touches only its completions (and, on
   // the wheel, entries a lap away), not every slot. Owner lanes retire in
