@@ -522,12 +522,16 @@ BFSIM_UNROLL_W
       double mxd = static_cast<double>(mx);
       double p = 0.0;
       unsigned long long smv = 0;
+      const double lmx = mx ? log2(mxd) : 0.0;
       for (int g = 0; g < G; ++g) {
         uint32_t L = row[g];
         smv += L;
-        // utilization u = L / max (metrics.hpp:56-62), power (metrics_power.hpp:24-27)
-        double u = mx ? __ddiv_rn(static_cast<double>(L), mxd) : 0.0;
-        p = __dadd_rn(p, __dadd_rn(p_idle, __dmul_rn(p_diff, pow(u, gam))));
+        // utilization u = L / max (metrics.hpp:56-62), power (metrics_power.hpp:24-27):
+        // u^gamma as 2^(gamma (log2 L - log2 max)) -- a few ulp from
+        // glibc's pow(L / max, gamma), far inside the 1e-9 energy bar; the
+        // idle (u = 0) and straggler (u = 1) workers are exact
+        const double pu = L == 0 ? 0.0 : (L == mx ? 1.0 : exp2(gam * (log2(static_cast<double>(L)) - lmx)));
+        p = __dadd_rn(p, __dadd_rn(p_idle, __dmul_rn(p_diff, pu)));
       }
       if (counted) {
         imb_l = static_cast<long long>(G) * mx - static_cast<long long>(smv);
