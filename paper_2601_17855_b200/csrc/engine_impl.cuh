@@ -195,8 +195,10 @@ struct ClassSet<true> {
   __device__ int highest() const { return bits ? 64 - __clzll(bits) : 0; }
   __device__ int lowest() const { return bits ? __ffsll(static_cast<long long>(bits)) : 0; }
   __device__ int highest_le(long long d) const {
-    uint64_t m = d >= 64 ? bits : (d < 1 ? 0ull : (bits & ((1ull << d) - 1ull)));
-    return m ? 64 - __clzll(m) : 0;
+    // classes 1..d are bits 0..d-1: shift them to the top, the rest falls off
+    if (d >= 64) return highest();
+    const uint64_t m = d < 1 ? 0ull : bits << (64 - static_cast<int>(d));
+    return m ? static_cast<int>(d) - __clzll(m) : 0;
   }
   __device__ void clear(int c) { bits &= ~(1ull << (c - 1)); }
   __device__ void add_from_lanes(bool has, int c) {
