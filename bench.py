@@ -238,15 +238,18 @@ def measured_peak():
 
 
 def ncu_traffic(config):
-    """dram bytes per launch of the dominant step kernel from the committed ncu capture."""
+    """dram bytes per launch of the dominant step kernel from the committed ncu
+    capture, plus that capture's issue-slot and warp activity (the kernel is
+    latency-bound: these say how far from issue-bound it is)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
         d = d.get(config, d if config == "c2" else {})
-        return d.get("dram_bytes_per_launch"), d.get("kernel")
+        return d.get("dram_bytes_per_launch"), d.get("kernel"), {
+            "issue_active": d.get("issue_active"), "warps_active": d.get("warps_active")}
     except Exception:
-        return None, None
+        return None, None, {}
 
 
 # --------------------------------------------------------------- CPU baseline
@@ -468,7 +471,7 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = measured_peak()
         achieved = dom_alg / (dom_ms / 1e3) / 1e9
-        traffic, traffic_kernel = ncu_traffic(args.config)
+        traffic, traffic_kernel, activity = ncu_traffic(args.config)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(wl, pool)
@@ -491,6 +494,7 @@ def run_ours(args):
                 "kernel": f"step_kernel family '{dom}' ({len(dom_idx)} trajectories, timed alone, CUDA events)",
                 "kernel_ms": dom_ms, "algorithmic_bytes": dom_alg, "peak_source": peak_src,
                 "traffic_source": traffic_kernel,
+                "ncu_activity": activity,
             },
             "per_family_kernel_ms": per_group,
             "cpu_baseline": cpu,
