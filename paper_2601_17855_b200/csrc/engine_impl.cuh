@@ -1285,10 +1285,11 @@ BFSIM_UNROLL_W
       // workers with a free slot (F3), one warp reduction per item
       key_t lk = lane_key(F0, cp);
       coop_init(F0, cp);
-      int cnext = o_c[0];
+      int cnext = o_c[0], cnext2 = U > 1 ? o_c[1] : 0;  // item classes, two ahead
       for (int j = 0; j < U; ++j) {
         const int c = cnext;
-        if (j + 1 < U) cnext = o_c[j + 1];
+        cnext = cnext2;
+        if (j + 2 < U) cnext2 = o_c[j + 2];
         const key_t km = wmin(lk);
         const int gs = static_cast<int>(km) & static_cast<int>(gmask);
         if constexpr (kCoop) {
@@ -1729,7 +1730,7 @@ BFSIM_UNROLL_W
             if (prev < 0) *hb = nx;
             else wnx[prev] = static_cast<uint16_t>(nx < 0 ? 0xFFFF : nx);
           }
-          const int g = slot_worker(slot);
+          const int g = WPL == 1 ? lane : slot_worker(slot);  // the walking lane owns the slot's worker
           const int i = slot - g * B;
           const int jj = g >> 5;
           const long long av = s_a[slot];
