@@ -29,6 +29,10 @@
  *                        extends the stream and re-runs (never user visible from
  *                        the C++ wrapper)
  *   BFSIM_ELIMIT      6  SearchLimitExceeded (bfio-exact, policies.hpp:174-178)
+ *   BFSIM_ERANGE      7  a GPU-path integer range was exceeded at run time (the
+ *                        per-slot a = s - drift*x is int32: drift * steps must stay
+ *                        below 2^31). No reference analogue (the reference's doubles
+ *                        lose exactness instead); std::overflow_error in the wrapper.
  *
  * A context is bound to one CUDA device and is not thread-safe: use one
  * context per host thread (the reference: one Simulation owns its state,
@@ -53,6 +57,7 @@ extern "C" {
 #define BFSIM_PARTIAL 4
 #define BFSIM_ESTREAM 5
 #define BFSIM_ELIMIT 6 /* bfio-exact: SearchLimitExceeded (policies.hpp:174-178), a std::runtime_error */
+#define BFSIM_ERANGE 7 /* GPU integer state range exceeded (drift * steps >= 2^31) */
 
 /* PolicyKind, policies.hpp:16 (same numbering). */
 #define BFSIM_POLICY_FCFS 0

@@ -35,6 +35,7 @@ inline void check(int rc, const char* err) {
   if (rc == BFSIM_OK || rc == BFSIM_PARTIAL) return;
   if (rc == BFSIM_EINVAL) throw std::invalid_argument(err);
   if (rc == BFSIM_ELOGIC) throw std::logic_error(err);
+  if (rc == BFSIM_ERANGE) throw std::overflow_error(err);
   throw std::runtime_error(std::string("bfsim_gpu: ") + err);
 }
 

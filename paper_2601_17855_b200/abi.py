@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import numpy as np
 
-OK, EINVAL, ELOGIC, ECUDA, PARTIAL, ESTREAM, ELIMIT = 0, 1, 2, 3, 4, 5, 6
+OK, EINVAL, ELOGIC, ECUDA, PARTIAL, ESTREAM, ELIMIT, ERANGE = 0, 1, 2, 3, 4, 5, 6, 7
 
 # PolicyKind, policies.hpp:16
 FCFS, JSQ, BFIO_EXACT, BFIO_GREEDY = 0, 1, 2, 3

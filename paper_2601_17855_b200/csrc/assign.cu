@@ -376,8 +376,8 @@ __global__ void __launch_bounds__(32) assign_kernel(AssignParams P) {
       // per-lane scratch: choice, best choice (n each), loads ((H+1)*G), caps, options (n+1)
       unsigned char* lw = ws + P.lane_offset + static_cast<size_t>(lane) * P.lane_stride;
       int32_t* lchoice = reinterpret_cast<int32_t*>(lw);
-      int32_t* bchoice = lchoice + P.n_max;
-      int32_t* lcap = bchoice + P.n_max;
+      int32_t* bchoice = lchoice + P.ex_n;
+      int32_t* lcap = bchoice + P.ex_n;
       int32_t* opt = lcap + 32;
       int64_t* L = reinterpret_cast<int64_t*>(lw + P.lane_i64_offset);
       exact(w, lchoice, bchoice, L, lcap, opt, P.limit, &P.cost[call], &P.status[call]);

@@ -11,6 +11,7 @@ struct AssignParams {
   const bfsim_assign_call_t* calls;
   int32_t n_calls;
   int32_t n_max, h_max;  // largest waiting list / horizon over the calls
+  int32_t ex_n;          // largest waiting list over the bfio-exact calls (lane scratch)
   const int64_t* previews;  // exact integer copies of the reference's doubles
   const int64_t* futures;
   const int32_t* caps;

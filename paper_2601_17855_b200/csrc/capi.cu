@@ -105,8 +105,10 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
   if (s.mode != BFSIM_MODE_POISSON && s.mode != BFSIM_MODE_OVERLOADED)
     return fail(err, errlen, BFSIM_EINVAL, "unknown mode");
   if (s.lookahead < 0 || s.lookahead > 2) return fail(err, errlen, BFSIM_EINVAL, "unknown lookahead");
-  if (s.lookahead == BFSIM_LOOKAHEAD_NOISY && !(s.noise_sigma >= 0.0 && s.noise_sigma < 1e300))
-    return fail(err, errlen, BFSIM_EINVAL, "noisy lookahead: bad noise_sigma");
+  // sigma <= 0 (or NaN) previews perfectly, as make_preview does (policies.hpp:74);
+  // an infinite sigma has no lround (the reference's result is undefined)
+  if (s.lookahead == BFSIM_LOOKAHEAD_NOISY && std::isinf(s.noise_sigma))
+    return fail(err, errlen, BFSIM_EINVAL, "noisy lookahead: infinite noise_sigma");
   if (s.input_id < 0 || s.input_id >= n_inputs)
     return fail(err, errlen, BFSIM_EINVAL, "scenario: input_id out of range");
   if (s.workers > 1024) return fail(err, errlen, BFSIM_EINVAL, "GPU path: workers > 1024 not supported");
@@ -132,6 +134,10 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
   if (lb >= 2147483647.0)
     return fail(err, errlen, BFSIM_EINVAL, "GPU path: per-worker load bound exceeds 2^31");
   if (in.max_decode >= (1 << 30)) return fail(err, errlen, BFSIM_EINVAL, "GPU path: decode too long");
+  // per-slot a = s - drift*x is int32 (Poisson runs check this per step: BFSIM_ERANGE)
+  if (s.mode == BFSIM_MODE_OVERLOADED &&
+      static_cast<double>(d) * static_cast<double>(s.warmup + s.steps) + in.s_max >= 2147483647.0)
+    return fail(err, errlen, BFSIM_EINVAL, "GPU path: drift * (warmup + steps) exceeds 2^31");
   return BFSIM_OK;
 }
 
@@ -720,6 +726,8 @@ int bfsim_run_batch(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen, int64_t n_sc
   }
   if (first == BFSIM_ESTREAM)
     return fail(err, errlen, BFSIM_ESTREAM, "overloaded sample stream exhausted");
+  if (first == BFSIM_ERANGE)
+    return fail(err, errlen, BFSIM_ERANGE, "GPU path: drift * step exceeded the int32 slot range (lower max_steps)");
   return first;
 }
 
@@ -735,6 +743,8 @@ int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64
   if (search_limit < 0) return fail(err, errlen, BFSIM_EINVAL, "search_limit < 0");
   cudaSetDevice(ctx->device);
   int n_max = 1, h_max = 0;
+  bool any_exact = false;
+  int ex_n = 1, ex_h = 0;  // bfio-exact's per-lane scratch bounds (n <= 64, H <= 16)
   auto int_ok = [](double v) { return v >= 0.0 && v < 2147483648.0 && v == std::floor(v); };
   for (int64_t k = 0; k < n_calls; ++k) {
     const auto& c = calls[k];
@@ -754,6 +764,9 @@ int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64
     for (int g = 0; g < c.workers; ++g) {
       if (caps[c.worker_offset + g] < 0 || active_counts[c.worker_offset + g] < 0)
         return fail(err, errlen, BFSIM_EINVAL, "assign call: negative cap or active_count");
+      // the fcfs / jsq argmax keys pack cap (20 bits) and count (26 bits) with the lane
+      if (caps[c.worker_offset + g] >= (1 << 20) || active_counts[c.worker_offset + g] >= (1 << 26))
+        return fail(err, errlen, BFSIM_EINVAL, "GPU assign: cap must be < 2^20 and active_count < 2^26");
       capsum += caps[c.worker_offset + g];
     }
     const int64_t U = std::min<int64_t>(c.n_waiting, capsum);
@@ -767,6 +780,11 @@ int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64
         return fail(err, errlen, BFSIM_EINVAL, "GPU assign: futures must be integers in [0, 2^31)");
     n_max = std::max(n_max, c.n_waiting);
     h_max = std::max(h_max, c.horizon);
+    if (c.policy == BFSIM_POLICY_BFIO_EXACT) {
+      any_exact = true;
+      ex_n = std::max(ex_n, c.n_waiting);
+      ex_h = std::max(ex_h, c.horizon);
+    }
   }
   std::vector<int64_t> pv(static_cast<size_t>(std::max<int64_t>(n_previews, 1)));
   std::vector<int64_t> fu(static_cast<size_t>(std::max<int64_t>(n_futures, 1)));
@@ -776,11 +794,13 @@ int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64
   ap.n_calls = static_cast<int32_t>(n_calls);
   ap.n_max = n_max;
   ap.h_max = h_max;
+  ap.ex_n = ex_n;
   auto al = [](int64_t x) { return (x + 15) & ~int64_t{15}; };
   ap.i64_offset = al(3LL * n_max * 4);
   ap.lane_offset = al(ap.i64_offset + (33LL * (h_max + 1)) * 8);
-  ap.lane_i64_offset = al((3LL * n_max + 33) * 4);
-  ap.lane_stride = al(ap.lane_i64_offset + (h_max + 1) * 32LL * 8);
+  // per-lane exact-search scratch only when a bfio-exact call is present
+  ap.lane_i64_offset = any_exact ? al((3LL * ex_n + 33) * 4) : 0;
+  ap.lane_stride = any_exact ? al(ap.lane_i64_offset + (ex_h + 1) * 32LL * 8) : 0;
   ap.ws_stride = al(ap.lane_offset + 32 * ap.lane_stride);
   ap.limit = search_limit;
   cudaStream_t us = nullptr;
@@ -793,7 +813,7 @@ int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64
   if ((e = up(ctx->a_calls, calls, n_calls * sizeof(bfsim_assign_call_t))) ||
       (e = up(ctx->a_pv, pv.data(), pv.size() * 8)) || (e = up(ctx->a_fut, fu.data(), fu.size() * 8)) ||
       (e = up(ctx->a_caps, caps, n_workers * 4)) || (e = up(ctx->a_cnt, active_counts, n_workers * 4)) ||
-      (e = ctx->a_pairs.ensure(std::max<int64_t>(n_pairs_cap, 1) * 4)) ||
+      (e = up(ctx->a_pairs, pairs, n_pairs_cap > 0 ? n_pairs_cap * 4 : 0)) ||
       (e = ctx->a_np.ensure(n_calls * 8)) || (e = ctx->a_cost.ensure(n_calls * 8)) ||
       (e = ctx->a_st.ensure(n_calls * 4)) || (e = ctx->a_ws.ensure(ap.ws_stride * n_calls)))
     return cuda_fail(err, errlen, e, "assign buffers");

@@ -314,7 +314,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   const int G = sc.workers, B = sc.batch;
   const int H = GREEDY ? sc.horizon : 0;
   const int Hm = H > 0 ? H : 1;  // modulus for the window ring (unused when H == 0)
-  const bool trunc = sc.lookahead == BFSIM_LOOKAHEAD_TRUNCATED;
+  // run_overloaded always previews perfectly (oracle.hpp:185-199)
+  const bool trunc = !OVL && sc.lookahead == BFSIM_LOOKAHEAD_TRUNCATED;
   const long long d = static_cast<long long>(sc.drift);
   const int S = in.s_max;
   const long long N = in.length;
@@ -449,6 +450,8 @@ BFSIM_UNROLL_W
       static_cast<long long>(B) * (static_cast<long long>(S) + d * (in.max_decode - 1));
   const bool k32 = bits_for(lbound) + gbits <= 31;
 
+  // a = s - d*x is kept in int32 per slot: steps beyond k_safe would wrap it
+  const long long k_safe = d > 0 ? (static_cast<long long>(INT_MAX) - S) / d : LLONG_MAX;
   long long k = 0;
   double clock = 0.0;
   long long nxt = 0, head = 0, n_wait = 0, act = 0, done = 0, tail = 0, adm_total = 0;
@@ -1784,6 +1787,10 @@ BFSIM_UNROLL_W
         status = BFSIM_PARTIAL;
         break;
       }
+    }
+    if (k > k_safe) {
+      status = BFSIM_ERANGE;
+      break;
     }
     const double cs = clock;
     if (OVL) {
