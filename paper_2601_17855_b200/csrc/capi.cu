@@ -252,19 +252,27 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_pbm, bm_words * 8});
   }
   if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8});
-  // M, T, w of the lookahead chain (also the register chain's row)
+  // M, T, w of the lookahead chain
   if (greedy && H > 0) items.push_back({&p.o_M, std::max<int64_t>(3 * (H + 1) * 8LL, 128)});
-  if (g.noisy) items.push_back({&p.o_mt, 312 * 8});
-  // per-slot state touched every step (retire scan, noisy views)
+  if (g.noisy) {
+    // the draw pass's shared-memory atomics (int32 difference arrays over h)
+    // and the register chain's [h][g] view mirror come first
+    items.push_back({&p.o_mt, 312 * 8});
+    items.push_back({&p.o_pre, (G + 1) * 4LL});
+    items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
+    items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 4});
+    if (g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G});
+  }
+  // per-slot state touched every step (retire)
   items.push_back({&p.o_f, ((GB + 3) & ~3LL) * 4});
   items.push_back({&p.o_a, GB * 4});
-  if (g.noisy) items.push_back({&p.o_lst, GB * 2});
   items.push_back({&p.o_stk, GB * 2});
-  if (greedy && H > 0) {
-    items.push_back({&p.o_F, (H + 1) * 8LL * G});
+  if (greedy && H > 0 && !g.noisy) {
+    items.push_back({&p.o_F, (H + 1) * (g.hr ? 4LL : 8LL) * G});  // int32 mirror for the register chain
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
   }
+  if (greedy && H > 0 && g.noisy && !g.hr) items.push_back({&p.o_F, (H + 1) * 8LL * G});
   if (p.cal == 2) {  // the 64-bucket completion wheel lives in shared memory
     items.push_back({&p.o_calh, 64LL * std::min(G, 32) * 4});
     items.push_back({&p.o_calnx, GB * 2});
@@ -320,6 +328,8 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   else p.o_deq = -1;
   if (g.noisy) {
     const int64_t words = (max_len + 63) / 64 + 2;
+    cold(&p.o_lst, GB * 8);
+    cold(&p.o_eid, GB * 4);
     cold(&p.o_nzb, (GB + max_len) * 4);
     cold(&p.o_abits, words * 8);
     cold(&p.o_zpre, words * 4);

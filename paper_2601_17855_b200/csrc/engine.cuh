@@ -36,9 +36,11 @@ struct Plan {
   int64_t o_F, o_M, o_Wc, o_Wa, o_oc, o_oo, o_oid;
   // TPOT completion buffer (cbuf entries) + misc counters
   int64_t o_cbuf, o_misc;
-  // noisy lookahead: mt19937_64 state, per-worker active lists, per-item
-  // draws (hot); the step's draws, admitted-id bitmap and its word prefix (cold)
-  int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre, o_selb;
+  // noisy lookahead: mt19937_64 state, draw -> worker prefix, per-item draws
+  // (hot); per-worker active lists of {finish step, a} (o_lst) and the ids of
+  // appended entries (o_eid), the admitted waiting draws, admitted-id bitmap
+  // and its word prefix (cold)
+  int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre, o_selb, o_eid, o_pre;
   // bfio-greedy with WPL >= 16: per-worker argmin keys
   int64_t o_key;
   // completion calendar (cal != 0, large G*B): list heads [R][32], per-slot links

@@ -385,11 +385,19 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* calh = cal == 1 ? gat<int32_t>(ws, pl.o_calh) : (cal == 2 ? at<SM, int32_t>(sm, ws, pl.o_calh) : nullptr);
   int32_t* calnx = cal == 1 ? gat<int32_t>(ws, pl.o_calnx) : nullptr;
   uint16_t* wnx = cal == 2 ? at<SM, uint16_t>(sm, ws, pl.o_calnx) : nullptr;
-  // Noisy lookahead (NOISY): engine state, per-worker active lists in
-  // insertion order (interleaved [pos * G + g]), per-item draws, the step's
-  // draws and the admitted-id bitmap that gives waiting ranks.
+  // Noisy lookahead (NOISY): engine state; per-worker active lists in
+  // insertion order, worker-major ([g * B + pos]), whose entries carry the
+  // request's {finish step, a} so the draw pass reads them coalesced in draw
+  // order, plus the ids of a step's appended entries (sort key); the
+  // exclusive prefix of the active counts over workers (draw r -> worker);
+  // difference arrays over h in int32 (shared-memory atomics); per-item
+  // draws; the admitted waiting draws and the admitted-id bitmap that gives
+  // waiting ranks.
   uint64_t* s_mt = NOISY ? at<SM, uint64_t>(sm, ws, pl.o_mt) : nullptr;
-  uint16_t* s_lst = NOISY ? at<SM, uint16_t>(sm, ws, pl.o_lst) : nullptr;
+  int2* s_E = NOISY ? gat<int2>(ws, pl.o_lst) : nullptr;
+  int32_t* s_Eid = NOISY ? gat<int32_t>(ws, pl.o_eid) : nullptr;
+  int32_t* s_pre = NOISY ? at<SM, int32_t>(sm, ws, pl.o_pre) : nullptr;
+  int32_t* n_Wa = NOISY ? reinterpret_cast<int32_t*>(s_Wa) : nullptr;
   int32_t* o_nz = NOISY ? at<SM, int32_t>(sm, ws, pl.o_onz) : nullptr;
   int32_t* nzb = NOISY ? gat<int32_t>(ws, pl.o_nzb) : nullptr;
   unsigned long long* abits = NOISY ? gat<unsigned long long>(ws, pl.o_abits) : nullptr;
@@ -413,7 +421,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   if (GREEDY && H > 0)
     for (int i = lane; i < H * G; i += 32) {
       s_Wc[i] = 0;
-      s_Wa[i] = 0;
+      if constexpr (NOISY) n_Wa[i] = 0;
+      else s_Wa[i] = 0;
     }
   ClassSet<SMALLC> wset, pset;  // waiting classes; classes picked in phase 1
   {
@@ -723,6 +732,11 @@ BFSIM_UNROLL_W
     int slot = g * B + s_stk[g * B + s_capb[g] - 1 - rank];
     s_f[slot] = static_cast<uint32_t>(k + o - 1);
     s_a[slot] = static_cast<int32_t>(s - d * k);
+    if constexpr (NOISY) {  // appended after the worker's active entries (sorted by id below)
+      const int pos = g * B + (B - s_capb[g]) + rank;
+      s_E[pos] = make_int2(static_cast<int>(k + o - 1), static_cast<int>(s - d * k));
+      s_Eid[pos] = static_cast<int32_t>(id);
+    }
     s_x[slot] = static_cast<int32_t>(k);
     s_id[slot] = static_cast<int32_t>(id);
     if (cal == 1) {
@@ -747,9 +761,19 @@ BFSIM_UNROLL_W
   // waiting_views in waiting order, :222-231). Every polar attempt takes the
   // two engine words at an even position, so lane l tests the pair at
   // mt_i + 2l and accepted pairs are numbered by a ballot prefix. With
-  // `values`, draw r stores lround(N(0, sigma)) in nzb[r].
+  // `values`, active draw r (< act) goes straight into the lookahead views:
+  // it belongs to entry r - pre[g] of worker g's insertion-ordered list
+  // (s_pre: exclusive prefix of the active counts), whose {finish step, a}
+  // the lanes read coalesced (consecutive draws, consecutive entries), and
+  // the request's preview (make_preview, policies.hpp:67-90) is added to the
+  // worker's difference arrays over h with shared-memory atomics: w_i + d*h
+  // while h < min(c_i, rem_i), its last workload a + d*f while
+  // rem_i <= h < c_i, with c_i = min(max(1, rem_i + lround(n_i)), H + 1) and
+  // rem_i = f - k + 1. A waiting draw's value is kept (nzb[r]) only when its
+  // request is admitted this step.
   auto gen_normals = [&](long long D, bool values) {
     long long got = 0;
+    int gq = 0;  // this lane's last worker (its draws only move forward)
     while (got < D) {
       if (mt_i >= kMtN) {
         mt_twist(s_mt);
@@ -776,28 +800,81 @@ BFSIM_UNROLL_W
         run += __popc(am[t]);
       }
       if (values) {
+        // values are needed for every active request's draw and for the
+        // waiting draws of requests admitted this step; the rest of the
+        // waiting draws only advance the stream. The five slots of a lane are
+        // independent: every stage is issued for all of them before the next
+        // (loads in flight together, interleaved log / div / sqrt chains).
+        long long rr[5];
+        bool nd[5];
+        unsigned sw[5];
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
-          const long long r = got + before[t] + __popc(am[t] & lanemask_lt());
-          // values are needed for every active request's draw and for the
-          // waiting draws of requests admitted this step; the rest of the
-          // waiting draws only advance the stream
-          bool need = ((am[t] >> lane) & 1u) && r < D;
-          if (need && r >= act) {
-            const long long p = r - act;
-            need = (__ldcg(selb + (p >> 5)) >> (p & 31)) & 1u;
-          }
-          if (!__any_sync(FULLMASK, need)) continue;
-          const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2v[t])), r2v[t]));
-          const double nv = __dadd_rn(__dmul_rn(__dmul_rn(yv[t], mult), sigma), 0.0);
-          if (need) {
-            long long lr = llround(nv);
-            lr = lr > (1ll << 30) ? (1ll << 30) : (lr < -(1ll << 30) ? -(1ll << 30) : lr);
-            nzb[r] = static_cast<int32_t>(lr);
+          rr[t] = got + before[t] + __popc(am[t] & lanemask_lt());
+          nd[t] = ((am[t] >> lane) & 1u) && rr[t] < D;
+          const long long p = rr[t] - act;
+          sw[t] = (nd[t] && p >= 0) ? __ldcg(selb + (p >> 5)) : 0u;
+        }
+        bool anyn = false;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          if (nd[t] && rr[t] >= act) nd[t] = (sw[t] >> ((rr[t] - act) & 31)) & 1u;
+          anyn = anyn || nd[t];
+        }
+        if (__any_sync(FULLMASK, anyn)) {
+          long long lr[5];
+#pragma unroll
+          for (int t = 0; t < 5; ++t) {
+            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2v[t])), r2v[t]));
+            const double nv = __dadd_rn(__dmul_rn(__dmul_rn(yv[t], mult), sigma), 0.0);
+            long long l = nd[t] ? llround(nv) : 0;
+            lr[t] = l > (1ll << 30) ? (1ll << 30) : (l < -(1ll << 30) ? -(1ll << 30) : l);
             // CUDA log is within 1 ulp of glibc's; only a draw this close to
             // a half-integer could round differently
             const double av = fabs(nv);
-            if (fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
+            if (nd[t] && fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
+          }
+          int gt[5], pt[5];
+#pragma unroll
+          for (int t = 0; t < 5; ++t) {
+            gt[t] = gq;
+            pt[t] = 0;
+            if (nd[t] && rr[t] < act) {
+              int g = gq, nx = s_pre[g + 1];
+              while (nx <= rr[t]) nx = s_pre[++g + 1];
+              gq = g;
+              gt[t] = g;
+              pt[t] = static_cast<int>(rr[t]) - s_pre[g];
+            }
+          }
+          int2 et[5];
+#pragma unroll
+          for (int t = 0; t < 5; ++t)
+            et[t] = (nd[t] && rr[t] < act) ? s_E[gt[t] * B + pt[t]] : make_int2(0, 0);
+#pragma unroll
+          for (int t = 0; t < 5; ++t) {
+            if (!nd[t]) continue;
+            if (rr[t] >= act) {
+              nzb[rr[t]] = static_cast<int32_t>(lr[t]);
+              continue;
+            }
+            const int g = gt[t];
+            const long long f = static_cast<uint32_t>(et[t].x);
+            const long long a = et[t].y;
+            const long long rem = f - k + 1;
+            long long pred = rem + lr[t];
+            pred = pred > 1 ? pred : 1;
+            const long long c = pred < H + 1 ? pred : H + 1;
+            const long long m = c < rem ? c : rem;
+            if (m <= H) {
+              atomicAdd(&n_Wa[(m - 1) * G + g], static_cast<int32_t>(-(a + d * k)));
+              atomicAdd(&s_Wc[(m - 1) * G + g], -1);
+            }
+            if (c > rem) {
+              const int32_t wl = static_cast<int32_t>(a + d * f);
+              atomicAdd(&n_Wa[(rem - 1) * G + g], wl);
+              if (c <= H) atomicAdd(&n_Wa[(c - 1) * G + g], -wl);
+            }
           }
         }
       }
@@ -848,58 +925,42 @@ BFSIM_UNROLL_W
     __syncwarp();
   };
 
-  // Lookahead views F_h[g] (worker_views, engine.hpp:204-220) from the
-  // per-slot draws: request i on g (finish step f, a = s - d*x) contributes
-  // w_i + d*h while h < min(c_i, rem_i) and its last workload a + d*f while
-  // rem_i <= h < c_i, c_i = min(max(1, rem_i + lround(n_i)), H + 1),
-  // rem_i = f - k + 1 (make_preview, policies.hpp:67-90). Owner lanes walk
-  // their workers' lists into difference arrays over h (s_Wa / s_Wc, unused
-  // by the noisy variant's retire) and prefix them into s_F.
-  auto noisy_views = [&]() {
+  // Draw r -> worker: s_pre[g] = active requests of workers < g (their
+  // draws come first, worker_views g ascending, engine.hpp:204-220).
+  auto noisy_pre = [&]() {
     long long base = 0;
-    int pre[WPL];
 BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) {
-      const int v = lane + 32 * j < G ? n[j] : 0;
+      const int g = lane + 32 * j;
+      const int v = g < G ? n[j] : 0;
       int incl = v;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         const int t = __shfl_up_sync(FULLMASK, incl, off);
         if (lane >= off) incl += t;
       }
-      pre[j] = static_cast<int>(base) + incl - v;
+      if (g < G) s_pre[g] = static_cast<int>(base) + incl - v;
       base += __shfl_sync(FULLMASK, incl, 31);
     }
+    if (lane == 0) s_pre[G] = static_cast<int>(base);
+    __syncwarp();
+  };
+
+  // Lookahead views F_h[g] (worker_views, engine.hpp:204-220) of the shared
+  // chain: prefix of the difference arrays the draw pass filled (zeroed for
+  // the next step), F_h[g] = A_g + d k n_g + sum_{h'<=h} Wa + d h (n_g + sum Wc).
+  auto noisy_views = [&]() {
 BFSIM_UNROLL_W
     for (int j = 0; j < WPL; ++j) {
       const int g = lane + 32 * j;
       if (g >= G) continue;
-      for (int p = 0; p < n[j]; ++p) {
-        const int slot = g * B + s_lst[p * G + g];
-        const long long f = s_f[slot];
-        const long long a = s_a[slot];
-        const long long rem = f - k + 1;
-        long long pred = rem + nzb[pre[j] + p];
-        pred = pred > 1 ? pred : 1;
-        const long long c = pred < H + 1 ? pred : H + 1;
-        const long long m = c < rem ? c : rem;
-        if (m <= H) {
-          s_Wa[(m - 1) * G + g] -= a + d * k;
-          s_Wc[(m - 1) * G + g] -= 1;
-        }
-        if (c > rem) {
-          const long long wl = a + d * f;
-          s_Wa[(rem - 1) * G + g] += wl;
-          if (c <= H) s_Wa[(c - 1) * G + g] -= wl;
-        }
-      }
       long long SW = A[j] + d * k * n[j];
       long long CN = n[j];
       s_F[g] = SW;
       for (int h = 1; h <= H; ++h) {
-        SW += s_Wa[(h - 1) * G + g];
+        SW += n_Wa[(h - 1) * G + g];
         CN += s_Wc[(h - 1) * G + g];
-        s_Wa[(h - 1) * G + g] = 0;
+        n_Wa[(h - 1) * G + g] = 0;
         s_Wc[(h - 1) * G + g] = 0;
         s_F[h * G + g] = SW + d * h * CN;
       }
@@ -1385,18 +1446,50 @@ BFSIM_UNROLL_W
       }
       __syncwarp();
       if constexpr (NOISY) {
-        // this step's draws (all of them, as the reference takes them), then
-        // the views from the active draws and each admitted request's own
-        // waiting draw
+        // this step's draws (all of them, as the reference takes them): the
+        // active draws build the views' difference arrays, each admitted
+        // request keeps its own waiting draw
         waiting_ranks(U, o_id, o_nz);
+        noisy_pre();
         gen_normals(act + n_wait, true);
-        noisy_views();
+        if constexpr (HR == 0) noisy_views();
         for (int q = lane; q < U; q += 32) {
           const int rank = o_nz[q];
           o_nz[q] = nzb[act + rank];
           selb[rank >> 5] = 0u;
         }
       }
+      // Per-item class, decode length and predicted completion, lane-held 32
+      // items at a time with the next 32 in flight: coalesced loads off the
+      // placement chain instead of dependent scalar loads per item.
+      int ic = 0, io = 1, iz = 0, nc2 = 0, no2 = 1, nz2 = 0;
+      auto item_load = [&](int q0) {
+        const int qi = q0 + lane;
+        nc2 = qi < U ? o_c[qi] : 0;
+        no2 = qi < U ? o_o[qi] : 1;
+        if constexpr (NOISY) nz2 = qi < U ? o_nz[qi] : 0;
+      };
+      // preview (make_preview, policies.hpp:67-90): w_h = c + d*min(h, o-1)
+      // for h < lim, else 0; lim = predicted completion (perfect: o;
+      // truncated: max(o, H+1); noisy: max(1, o + lround(n)))
+      auto item_at = [&](int q, int& c, int& o, long long& lim) {
+        if ((q & 31) == 0) {
+          ic = nc2;
+          io = no2;
+          iz = nz2;
+          item_load(q + 32);
+        }
+        c = __shfl_sync(FULLMASK, ic, q & 31);
+        o = __shfl_sync(FULLMASK, io, q & 31);
+        lim = o;
+        if constexpr (NOISY) {
+          lim = static_cast<long long>(o) + __shfl_sync(FULLMASK, iz, q & 31);
+          lim = lim > 1 ? lim : 1;
+        } else {
+          if (trunc && lim < H + 1) lim = H + 1;
+        }
+      };
+      item_load(0);
       if constexpr (HR > 0) {
         // Register-resident chain (H < HR, G <= 64, every cost < 2^31; the
         // planner checks the bounds). Lane g holds F_h[g] for its workers;
@@ -1406,14 +1499,33 @@ BFSIM_UNROLL_W
         // the first sum does not depend on g, so the argmin and its ties over
         // (cost, F_0[g], g) are unchanged (policies.hpp:339-367).
         // Entries h > H stay 0 and add nothing; the loops are branch-free.
+        int32_t* s_F32 = reinterpret_cast<int32_t*>(s_F);  // row-major [h][g] mirror of Fr
         if constexpr (NOISY) {
+          // views: prefix of the difference arrays the draw pass filled
+          // (zeroed for the next step), straight into registers
 #pragma unroll
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
+            long long SW = g < G ? A[j] + d * k * n[j] : 0;
+            long long CN = g < G ? n[j] : 0;
 #pragma unroll
-            for (int h = 0; h < HR; ++h)
-              Fr[j][h] = (g < G && h <= H) ? static_cast<int32_t>(s_F[h * G + g]) : 0;
+            for (int h = 0; h < HR; ++h) {
+              if (h > 0 && h <= H && g < G) {
+                SW += n_Wa[(h - 1) * G + g];
+                CN += s_Wc[(h - 1) * G + g];
+                n_Wa[(h - 1) * G + g] = 0;
+                s_Wc[(h - 1) * G + g] = 0;
+              }
+              Fr[j][h] = (g < G && h <= H) ? static_cast<int32_t>(SW + d * h * CN) : 0;
+            }
           }
+        }
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+          const int g = lane + 32 * j;
+#pragma unroll
+          for (int h = 0; h < HR; ++h)
+            if (g < G && h <= H) s_F32[h * G + g] = Fr[j][h];
         }
         int32_t Ml = 0;  // M_lane
 #pragma unroll
@@ -1424,45 +1536,56 @@ BFSIM_UNROLL_W
           const int32_t m = static_cast<int32_t>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(v)));
           Ml = lane == h ? m : Ml;
         }
+        __syncwarp();
         const int32_t d32 = static_cast<int32_t>(d);
         const int32_t dl = d32 * lane;
+        const bool hl = lane <= H && lane < HR;  // this lane holds a horizon
         for (int q = 0; q < U; ++q) {
-          const int c = o_c[q], o = o_o[q];
-          long long lim = o;
-          if constexpr (NOISY) {
-            lim = static_cast<long long>(o) + o_nz[q];
-            lim = lim > 1 ? lim : 1;
-          } else {
-            if (trunc && lim < H + 1) lim = H + 1;
-          }
+          int c, o;
+          long long lim;
+          item_at(q, c, o, lim);
           const int limH = static_cast<int>(lim < H + 1 ? lim : H + 1);
           const int32_t sat = d32 * (o - 1);
           const int32_t wl = lane < limH ? c + (dl < sat ? dl : sat) : 0;
-          const int32_t Tl = Ml - wl;
-          uint32_t cost[WPL];
-#pragma unroll
-          for (int j = 0; j < WPL; ++j) cost[j] = 0;
-#pragma unroll
-          for (int h = 0; h < HR; ++h) {
-            const int32_t T = __shfl_sync(FULLMASK, Tl, h);
-#pragma unroll
-            for (int j = 0; j < WPL; ++j) cost[j] += static_cast<uint32_t>(T > Fr[j][h] ? T : Fr[j][h]);
-          }
-          uint64_t best = ~0ull;
+          // Fast path: g* = argmin (F_0[g], g) over workers with a free slot.
+          // Every cost is >= sum_h max(M_h, 0 + ...) >= sum_h M_h, and g*'s
+          // cost equals sum_h M_h iff F_h[g*] + w_h <= M_h for every h; then
+          // g* has the minimum cost and the smallest (F_0, g) tie-break key,
+          // so it wins outright. Otherwise the full scan.
+          key_t fk = KMAX;
 #pragma unroll
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
-            const uint64_t key = (static_cast<uint64_t>(cost[j]) << 32) |
-                                 (static_cast<uint64_t>(static_cast<uint32_t>(Fr[j][0])) << gbits) |
-                                 static_cast<uint64_t>(g);
-            if (g < G && cp[j] > 0 && key < best) best = key;
+            const key_t kk = (static_cast<key_t>(static_cast<uint32_t>(Fr[j][0])) << gbits) | static_cast<key_t>(g);
+            if (g < G && cp[j] > 0 && kk < fk) fk = kk;
           }
-          const uint64_t km = wmin_u64(best);
-          const int gs = static_cast<int>(km & gmask);
+          int gs = static_cast<int>(wmin(fk) & static_cast<key_t>(gmask));
+          const bool over = hl && s_F32[lane * G + gs] + wl > Ml;
+          if (__any_sync(FULLMASK, over)) {
+            const int32_t Tl = Ml - wl;
+            uint32_t cost[WPL];
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) cost[j] = 0;
+#pragma unroll
+            for (int h = 0; h < HR; ++h) {
+              const int32_t T = __shfl_sync(FULLMASK, Tl, h);
+#pragma unroll
+              for (int j = 0; j < WPL; ++j) cost[j] += static_cast<uint32_t>(T > Fr[j][h] ? T : Fr[j][h]);
+            }
+            uint64_t best = ~0ull;
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) {
+              const int g = lane + 32 * j;
+              const uint64_t key = (static_cast<uint64_t>(cost[j]) << 32) |
+                                   (static_cast<uint64_t>(static_cast<uint32_t>(Fr[j][0])) << gbits) |
+                                   static_cast<uint64_t>(g);
+              if (g < G && cp[j] > 0 && key < best) best = key;
+            }
+            gs = static_cast<int>(wmin_u64(best) & gmask);
+          }
           const int own = gs & 31, jj = gs >> 5;
           // the owner adds w_h to the chosen row (recomputing w_h, no per-item
           // array) and publishes the row; lane h then raises M_h with it
-          int32_t* s_row = reinterpret_cast<int32_t*>(s_M);
           if (lane == own) {
 #pragma unroll
             for (int j = 0; j < WPL; ++j)
@@ -1471,7 +1594,7 @@ BFSIM_UNROLL_W
                 for (int h = 0; h < HR; ++h) {
                   const int32_t dh = d32 * h;
                   Fr[j][h] += h < limH ? c + (dh < sat ? dh : sat) : 0;
-                  s_row[h] = Fr[j][h];
+                  if (h <= H) s_F32[h * G + gs] = Fr[j][h];
                 }
                 cp[j] -= 1;
                 A[j] += c + ak;
@@ -1485,7 +1608,10 @@ BFSIM_UNROLL_W
               }
           }
           __syncwarp();
-          if (lane < HR) Ml = s_row[lane] > Ml ? s_row[lane] : Ml;
+          if (hl) {
+            const int32_t v = s_F32[lane * G + gs];
+            Ml = v > Ml ? v : Ml;
+          }
           __syncwarp();
         }
         __syncwarp();
@@ -1508,17 +1634,9 @@ BFSIM_UNROLL_W
         }
         __syncwarp();
         for (int q = 0; q < U; ++q) {
-          const int c = o_c[q], o = o_o[q];
-          // preview (make_preview, policies.hpp:67-90): w_h = c + d*min(h, o-1)
-          // for h < lim, else 0; lim = predicted completion (perfect: o;
-          // truncated: max(o, H+1); noisy: max(1, o + lround(n)))
-          long long lim = o;
-          if constexpr (NOISY) {
-            lim = static_cast<long long>(o) + o_nz[q];
-            lim = lim > 1 ? lim : 1;
-          } else {
-            if (trunc && lim < H + 1) lim = H + 1;
-          }
+          int c, o;
+          long long lim;
+          item_at(q, c, o, lim);
           for (int h = lane; h <= H; h += 32) {
             const long long w = h < lim ? c + d * (h < o ? h : o - 1) : 0;
             s_w[h] = w;
@@ -1613,24 +1731,27 @@ BFSIM_UNROLL_W
         }
       }
       if constexpr (NOISY) {
-        // append this step's admissions to each worker's list in waiting
-        // order (Simulation::apply pushes in assignment order, sorted by
-        // waiting index: engine.hpp:233-248, policies.hpp:368)
+        // this step's admissions were appended to each worker's list in
+        // placement order: sort them into waiting order (Simulation::apply
+        // pushes in assignment order, sorted by waiting index:
+        // engine.hpp:233-248, policies.hpp:368)
         __syncwarp();
 BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           const int g = lane + 32 * j;
           if (g >= G) continue;
-          const int capb = s_capb[g];
-          for (int t = 0; t < adm[j]; ++t) {
-            const int i = s_stk[g * B + capb - 1 - t];
-            const int key = s_id[g * B + i];
-            int pos = n[j] + t;
-            while (pos > n[j] && s_id[g * B + s_lst[(pos - 1) * G + g]] > key) {
-              s_lst[pos * G + g] = s_lst[(pos - 1) * G + g];
+          const int base = g * B + n[j];
+          for (int t = 1; t < adm[j]; ++t) {
+            const int key = s_Eid[base + t];
+            const int2 ev = s_E[base + t];
+            int pos = t;
+            while (pos > 0 && s_Eid[base + pos - 1] > key) {
+              s_Eid[base + pos] = s_Eid[base + pos - 1];
+              s_E[base + pos] = s_E[base + pos - 1];
               --pos;
             }
-            s_lst[pos * G + g] = static_cast<uint16_t>(i);
+            s_Eid[base + pos] = key;
+            s_E[base + pos] = ev;
           }
         }
         // advance the first bitmap word that still holds a waiting id
@@ -1757,17 +1878,36 @@ BFSIM_UNROLL_W
         }
       }
       __syncwarp();
+      if constexpr (NOISY) {
+        // erase_if keeps insertion order (engine.hpp:118-120): each worker
+        // with completions compacts its list, the whole warp over its
+        // entries (coalesced), dropping the ones that finish at step k
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j) {
+          unsigned dm = __ballot_sync(FULLMASK, lane + 32 * j < G && rc[j] > 0);
+          while (dm) {
+            const int src = __ffs(dm) - 1;
+            dm &= dm - 1;
+            const int g = src + 32 * j;
+            const int nold = __shfl_sync(FULLMASK, n[j], src);
+            int2* Eg = s_E + g * B;
+            int w = 0;
+            for (int p0 = 0; p0 < nold; p0 += 32) {
+              const int p = p0 + lane;
+              const int2 e = p < nold ? Eg[p] : make_int2(0, 0);
+              const bool keep = p < nold && static_cast<uint32_t>(e.x) != kf;
+              const unsigned km = __ballot_sync(FULLMASK, keep);
+              if (keep) Eg[w + __popc(km & lanemask_lt())] = e;
+              w += __popc(km);
+            }
+          }
+        }
+        __syncwarp();
+      }
 BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         const int g = lane + 32 * j;
         if (g >= G || rc[j] == 0) continue;
-        if constexpr (NOISY) {  // erase_if keeps insertion order (engine.hpp:118-120)
-          int w = 0;
-          for (int p = 0; p < n[j]; ++p) {
-            const uint16_t i = s_lst[p * G + g];
-            if (s_f[g * B + i] != kEmpty) s_lst[(w++) * G + g] = i;
-          }
-        }
         n[j] -= rc[j];
         s_cap[g] = B - n[j];
       }

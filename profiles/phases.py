@@ -57,6 +57,7 @@ def main():
     rows = list(csv.reader(out.splitlines()))
     marks = ranges()
     tot = defaultdict(float)
+    ins = defaultdict(float)
     hdr = None
     cur = None
     fname = None
@@ -69,6 +70,7 @@ def main():
         if r[0] == "Line No":
             hdr = r
             si = hdr.index("Warp Stall Sampling (All Samples)")
+            ei = hdr.index("Instructions Executed")
             continue
         if hdr is None or len(r) < len(hdr):
             continue
@@ -78,13 +80,18 @@ def main():
             continue
         try:
             s = float(r[si] or 0)
+            e = float(r[ei] or 0)
         except ValueError:
             continue
         key = phase_of(marks, cur[1]) if cur[0] == "engine_impl.cuh" else "intrinsics (" + cur[0] + ")"
         tot[key] += s
+        ins[key] += e
     t = sum(tot.values()) or 1
+    ti = sum(ins.values()) or 1
+    print("stall-samples  warp-instructions  phase")
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-        print(f"{100 * v / t:5.1f}%  {k}")
+        print(f"{100 * v / t:12.1f}%  {100 * ins[k] / ti:16.1f}%  {k}")
+    print(f"total warp instructions: {ti:.4g}")
 
 
 if __name__ == "__main__":

@@ -1,0 +1,136 @@
+"""Oracle parity at the shapes the benchmark runs (VERDICT r1 "what's weak" #1).
+
+* C4's stated shape: run_overloaded with G in {256, 512, 1024}, B = 64, each
+  of {fcfs, jsq, bfio-greedy H=0 at drift 0, bfio-greedy H=20 at drift 1}
+  (oracle.hpp:138-244, policies.hpp:339-367), on a 20 + 100 step prefix of the
+  2000 + 200 step runs. This exercises the wide-G code paths the bench times:
+  32-worker-per-lane registers in local memory, cooperative argmin keys
+  (G > 256), the shared-memory lookahead chain, and the exact-bucket
+  completion calendar at 65,536 slots.
+* C5's noisy family: a whole 1M-request C5 trace (lambda = 8000/s x 125 s)
+  under bfio-greedy H=20 Noisy sigma=2, G = B = 64, to completion; and a
+  1M-request trace at lambda = 16000/s whose waiting queue passes 100k, so
+  the admitted-id / admitted-rank bitmaps and the O(|waiting|) draws per step
+  (engine.hpp:222-231) run at fleet depth.
+
+Compared with the CPU oracle (pinned to the reference build in
+tests/test_oracle_vs_ref.py): every step record, every request's start step,
+worker and clocks, and the MetricsReport (exact fields bit-exact, energy and
+TPOT within 1e-9 relative)."""
+import numpy as np
+import pytest
+
+from paper_2601_17855_b200 import abi, host
+
+pytestmark = pytest.mark.gpu
+
+EXACT = ("avg_imbalance", "throughput", "imb_total", "total_workload", "eta_sum")
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = host.Context(0)
+    yield c
+    c.close()
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(a), abs(b), 1e-300)
+
+
+def _metrics_match(g, res):
+    for k in ("imb_total_i", "total_workload_i", "tokens_i", "records", "completed", "steps_run"):
+        assert int(g[k]) == int(res[k]), k
+    for k in EXACT:
+        assert float(g[k]) == float(res[k]), k
+    for k in ("energy", "tpot"):
+        assert _rel(float(g[k]), float(res[k])) <= TOL, (k, float(g[k]), float(res[k]))
+
+
+@pytest.mark.parametrize("G", [256, 512, 1024])
+def test_c4_stated_shape_prefix(ctx, orc, G):
+    B, steps, warm, p = 64, 100, 20, 0.02
+    n = int(G * B * (2 + (steps + warm) * p * 1.3)) + 8192
+    stream = host.sample_stream(7, n, s_max=64, p=p)
+    combos = ((abi.FCFS, 0, 0.0), (abi.JSQ, 0, 0.0), (abi.BFIO_GREEDY, 0, 0.0), (abi.BFIO_GREEDY, 20, 1.0))
+    rows = [abi.scenario(mode=abi.OVERLOADED, policy=pol, workers=G, batch=B, horizon=H, drift=d, steps=steps,
+                         warmup=warm, seed=7, input_id=0) for pol, H, d in combos]
+    br = ctx.run_batch(np.array(rows, abi.scenario_dtype), host.InputPool([stream]), emit_steps=True,
+                       emit_requests=True)
+    for i in range(len(rows)):
+        rc, res, st, per, tm = orc.run_overloaded(br.scen[i], stream, 64)
+        g = br.res[i]
+        assert int(g["status"]) == abi.OK
+        assert int(g["consumed"]) == int(res["consumed"])
+        gs = br.steps(i)
+        assert gs["loads"].shape == (steps, G)
+        np.testing.assert_array_equal(gs["loads"], st.loads)
+        np.testing.assert_array_equal(gs["dt"], st.dt)
+        np.testing.assert_array_equal(gs["clock_start"], st.clock_start)
+        np.testing.assert_array_equal(gs["active_count"], st.active_count)
+        assert (gs["active_count"] == G * B).all()  # full batches after warm-up (oracle_test.cpp:99-107)
+        m = int(res["consumed"])
+        gr = br.requests(i, stream.shape[0])
+        np.testing.assert_array_equal(gr["start_step"][:m], per["start_step"][:m])
+        np.testing.assert_array_equal(gr["worker"][:m], per["worker"][:m])
+        _metrics_match(g, res)
+    # JSQ == FCFS bit for bit
+    np.testing.assert_array_equal(br.steps(0)["loads"], br.steps(1)["loads"])
+
+
+def _poisson_full(ctx, orc, tr, sc, status=abi.OK):
+    br = ctx.run_batch(np.array([sc], abi.scenario_dtype), host.InputPool([tr]), emit_steps=True,
+                       emit_requests=True)
+    rc, res, st, rq = orc.run_poisson(br.scen[0], tr)
+    g = br.res[0]
+    assert int(g["status"]) == int(res["status"]) == status
+    assert not int(g["flags"]) & abi.FLAG_NOISE_NEAR_TIE
+    gs = br.steps(0)
+    for k in ("loads", "dt", "clock_start", "max_load", "active_count"):
+        np.testing.assert_array_equal(gs[k], getattr(st, k), err_msg=k)
+    gr = br.requests(0, tr.shape[0])
+    for k in ("arrival_step", "start_step", "worker", "admit_clock", "finish_clock"):
+        np.testing.assert_array_equal(gr[k], rq[k], err_msg=k)
+    assert float(g["clock"]) == float(res["clock"])
+    _metrics_match(g, res)
+    return gr
+
+
+def _max_waiting(rq, K):
+    """Largest waiting queue over the run: revealed (arrival step <= k) and
+    not yet admitted (start step > k)."""
+    arr = rq["arrival_step"].astype(np.int64)
+    st = rq["start_step"].astype(np.int64)
+    d = np.zeros(K + 2, np.int64)
+    rev = arr >= 0
+    np.add.at(d, arr[rev], 1)
+    adm = st >= 0
+    np.add.at(d, st[adm], -1)
+    return int(np.cumsum(d).max())
+
+
+def test_c5_noisy_full_trace(ctx, orc):
+    """A whole C5 trace (seed 1, ~1M requests) under the C5 grid's noisy
+    family: bfio-greedy H=20, Noisy sigma=2, G=B=64, simulated to completion."""
+    tr = host.sample_instance(1, rate=8000.0, duration=125.0, s_max=64, p=0.02)
+    assert tr.shape[0] > 990_000
+    sc = abi.scenario(policy=abi.BFIO_GREEDY, workers=64, batch=64, horizon=20, lookahead=abi.NOISY,
+                      noise_sigma=2.0, seed=1, drift=1.0, input_id=0)
+    gr = _poisson_full(ctx, orc, tr, sc)
+    assert (gr["finish_clock"] > 0).all()
+
+
+def test_c5_noisy_deep_waiting_queue(ctx, orc):
+    """A 1M-request trace at lambda = 16000/s (twice the G=B=64 service rate)
+    on a 1,500-step prefix (max_steps: a partial run, engine.hpp:173): the
+    waiting queue passes 100k, so every late step draws >100k normals
+    (engine.hpp:222-231) and admitted ranks come from the million-bit
+    admitted-id bitmap."""
+    tr = host.sample_instance(2, rate=16000.0, duration=62.5, s_max=64, p=0.02)
+    assert tr.shape[0] > 990_000
+    K = 1500
+    sc = abi.scenario(policy=abi.BFIO_GREEDY, workers=64, batch=64, horizon=20, lookahead=abi.NOISY,
+                      noise_sigma=2.0, seed=2, drift=1.0, input_id=0, max_steps=K)
+    gr = _poisson_full(ctx, orc, tr, sc, status=abi.PARTIAL)
+    assert _max_waiting(gr, K) > 100_000
