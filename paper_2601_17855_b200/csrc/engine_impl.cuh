@@ -822,17 +822,41 @@ BFSIM_UNROLL_W
           anyn = anyn || nd[t];
         }
         if (__any_sync(FULLMASK, anyn)) {
+          // lround(y * sqrt(-2 ln r2 / r2) * sigma) is an integer: a float
+          // estimate decides it unless the value lies within 1e-5 (relative)
+          // of a half-integer. The estimate's error is below 1e-6 relative:
+          // -ln r2 as -log1pf(r2 - 1) (r2 - 1 exact in double) or -logf(r2),
+          // each within 1 ulp and ~2.2 ulp after the input rounding, then
+          // IEEE division, sqrt and products (no fast-math): ~10 ulp of 2^-24
+          // in all. Those rare draws take the reference's double-precision
+          // formula (the previous, exact path).
+          const float sf = static_cast<float>(sigma);
           long long lr[5];
+          bool ex[5];
+          bool anyex = false;
 #pragma unroll
           for (int t = 0; t < 5; ++t) {
-            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2v[t])), r2v[t]));
-            const double nv = __dadd_rn(__dmul_rn(__dmul_rn(yv[t], mult), sigma), 0.0);
-            long long l = nd[t] ? llround(nv) : 0;
-            lr[t] = l > (1ll << 30) ? (1ll << 30) : (l < -(1ll << 30) ? -(1ll << 30) : l);
-            // CUDA log is within 1 ulp of glibc's; only a draw this close to
-            // a half-integer could round differently
-            const double av = fabs(nv);
-            if (nd[t] && fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
+            const float r2f = static_cast<float>(r2v[t]);
+            const float L = r2v[t] < 0.25 ? -logf(r2f) : -log1pf(static_cast<float>(r2v[t] - 1.0));
+            const float nf = static_cast<float>(yv[t]) * sqrtf(2.0f * L / r2f) * sf;
+            const float af = fabsf(nf);
+            ex[t] = nd[t] && (!(af < 1048576.0f) || fabsf((af - floorf(af)) - 0.5f) <= 1e-5f * fmaxf(1.0f, af));
+            lr[t] = nd[t] && !ex[t] ? static_cast<long long>(lroundf(nf)) : 0;
+            anyex = anyex || ex[t];
+          }
+          if (__any_sync(FULLMASK, anyex)) {
+#pragma unroll
+            for (int t = 0; t < 5; ++t) {
+              if (!ex[t]) continue;
+              const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2v[t])), r2v[t]));
+              const double nv = __dadd_rn(__dmul_rn(__dmul_rn(yv[t], mult), sigma), 0.0);
+              const long long l = llround(nv);
+              lr[t] = l > (1ll << 30) ? (1ll << 30) : (l < -(1ll << 30) ? -(1ll << 30) : l);
+              // CUDA log is within 1 ulp of glibc's; only a draw this close
+              // to a half-integer could round differently
+              const double av = fabs(nv);
+              if (fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
+            }
           }
           int gt[5], pt[5];
 #pragma unroll
@@ -1391,28 +1415,26 @@ BFSIM_UNROLL_W
       }
     } else {
       // general H: lookahead views F_h[g] from the finish window
-      // (HR > 0: held in registers Fr[j][h], h < HR, for the chain below)
-      int32_t Fr[WPL][HR > 0 ? HR : 1];
+      // (HR > 0: int32 views F_h[g] in shared memory, row-major [h][g], for
+      // the chain below)
+      int32_t* s_F32 = reinterpret_cast<int32_t*>(s_F);
       if constexpr (!NOISY && HR > 0) {
-#pragma unroll
+BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           const int g = lane + 32 * j;
+          if (g >= G) continue;
           long long PA = 0, PC = 0, Q = 0;
           int r = static_cast<int>(k % Hm);  // ring row of step k + h - 1
-#pragma unroll
-          for (int h = 0; h < (HR > 0 ? HR : 1); ++h) {
-            long long F = 0;
-            if (h <= H && g < G) {
-              if (h > 0) {
-                PA += s_Wa[r * G + g];
-                PC += s_Wc[r * G + g];
-                Q += PC;
-                r = r + 1 == Hm ? 0 : r + 1;
-              }
-              const long long kh = k + h;
-              F = trunc ? A[j] + d * kh * n[j] - d * Q : (A[j] + d * kh * n[j]) - (PA + d * kh * PC);
+          for (int h = 0; h <= H; ++h) {
+            if (h > 0) {
+              PA += s_Wa[r * G + g];
+              PC += s_Wc[r * G + g];
+              Q += PC;
+              r = r + 1 == Hm ? 0 : r + 1;
             }
-            Fr[j][h] = static_cast<int32_t>(F);
+            const long long kh = k + h;
+            const long long F = trunc ? A[j] + d * kh * n[j] - d * Q : (A[j] + d * kh * n[j]) - (PA + d * kh * PC);
+            s_F32[h * G + g] = static_cast<int32_t>(F);
           }
         }
       }
@@ -1491,55 +1513,45 @@ BFSIM_UNROLL_W
       };
       item_load(0);
       if constexpr (HR > 0) {
-        // Register-resident chain (H < HR, G <= 64, every cost < 2^31; the
-        // planner checks the bounds). Lane g holds F_h[g] for its workers;
-        // lane h holds M_h = max_g F_h[g] and, per item, w_h and
-        // T_h = M_h - w_h. The placement cost of worker g is
+        // int32 chain (H < HR <= 24, G <= 128, every cost < 2^31; the planner
+        // checks the bounds). F_h[g] lives in shared memory ([h][g]); lane h
+        // holds M_h = max_g F_h[g] and, per item, w_h and T_h = M_h - w_h;
+        // lane g holds F_0 of its workers. The placement cost of worker g is
         // sum_h max(M_h, F_h[g] + w_h) = sum_h w_h + sum_h max(T_h, F_h[g]);
         // the first sum does not depend on g, so the argmin and its ties over
         // (cost, F_0[g], g) are unchanged (policies.hpp:339-367).
-        // Entries h > H stay 0 and add nothing; the loops are branch-free.
-        int32_t* s_F32 = reinterpret_cast<int32_t*>(s_F);  // row-major [h][g] mirror of Fr
         if constexpr (NOISY) {
           // views: prefix of the difference arrays the draw pass filled
-          // (zeroed for the next step), straight into registers
-#pragma unroll
+          // (zeroed for the next step)
+BFSIM_UNROLL_W
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
-            long long SW = g < G ? A[j] + d * k * n[j] : 0;
-            long long CN = g < G ? n[j] : 0;
-#pragma unroll
-            for (int h = 0; h < HR; ++h) {
-              if (h > 0 && h <= H && g < G) {
-                SW += n_Wa[(h - 1) * G + g];
-                CN += s_Wc[(h - 1) * G + g];
-                n_Wa[(h - 1) * G + g] = 0;
-                s_Wc[(h - 1) * G + g] = 0;
-              }
-              Fr[j][h] = (g < G && h <= H) ? static_cast<int32_t>(SW + d * h * CN) : 0;
+            if (g >= G) continue;
+            long long SW = A[j] + d * k * n[j];
+            long long CN = n[j];
+            s_F32[g] = static_cast<int32_t>(SW);
+            for (int h = 1; h <= H; ++h) {
+              SW += n_Wa[(h - 1) * G + g];
+              CN += s_Wc[(h - 1) * G + g];
+              n_Wa[(h - 1) * G + g] = 0;
+              s_Wc[(h - 1) * G + g] = 0;
+              s_F32[h * G + g] = static_cast<int32_t>(SW + d * h * CN);
             }
           }
         }
-#pragma unroll
-        for (int j = 0; j < WPL; ++j) {
-          const int g = lane + 32 * j;
-#pragma unroll
-          for (int h = 0; h < HR; ++h)
-            if (g < G && h <= H) s_F32[h * G + g] = Fr[j][h];
-        }
-        int32_t Ml = 0;  // M_lane
-#pragma unroll
-        for (int h = 0; h < HR; ++h) {
-          int32_t v = 0;
-#pragma unroll
-          for (int j = 0; j < WPL; ++j) v = Fr[j][h] > v ? Fr[j][h] : v;
-          const int32_t m = static_cast<int32_t>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(v)));
-          Ml = lane == h ? m : Ml;
-        }
         __syncwarp();
+        const bool hl = lane <= H;  // this lane holds horizon h = lane
+        int32_t Ml = 0;              // M_lane
+        if (hl)
+          for (int g = 0; g < G; ++g) {
+            const int32_t v = s_F32[lane * G + g];
+            Ml = v > Ml ? v : Ml;
+          }
+        int32_t F0r[WPL];
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j) F0r[j] = lane + 32 * j < G ? s_F32[lane + 32 * j] : 0;
         const int32_t d32 = static_cast<int32_t>(d);
         const int32_t dl = d32 * lane;
-        const bool hl = lane <= H && lane < HR;  // this lane holds a horizon
         for (int q = 0; q < U; ++q) {
           int c, o;
           long long lim;
@@ -1548,69 +1560,68 @@ BFSIM_UNROLL_W
           const int32_t sat = d32 * (o - 1);
           const int32_t wl = lane < limH ? c + (dl < sat ? dl : sat) : 0;
           // Fast path: g* = argmin (F_0[g], g) over workers with a free slot.
-          // Every cost is >= sum_h max(M_h, 0 + ...) >= sum_h M_h, and g*'s
-          // cost equals sum_h M_h iff F_h[g*] + w_h <= M_h for every h; then
-          // g* has the minimum cost and the smallest (F_0, g) tie-break key,
-          // so it wins outright. Otherwise the full scan.
+          // Every cost is >= sum_h M_h, and g*'s cost equals it iff
+          // F_h[g*] + w_h <= M_h for every h; then g* has the minimum cost
+          // and the smallest (F_0, g) tie-break key, so it wins outright.
+          // Otherwise the full scan over every worker.
           key_t fk = KMAX;
-#pragma unroll
+BFSIM_UNROLL_W
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
-            const key_t kk = (static_cast<key_t>(static_cast<uint32_t>(Fr[j][0])) << gbits) | static_cast<key_t>(g);
+            const key_t kk = (static_cast<key_t>(static_cast<uint32_t>(F0r[j])) << gbits) | static_cast<key_t>(g);
             if (g < G && cp[j] > 0 && kk < fk) fk = kk;
           }
           int gs = static_cast<int>(wmin(fk) & static_cast<key_t>(gmask));
-          const bool over = hl && s_F32[lane * G + gs] + wl > Ml;
-          if (__any_sync(FULLMASK, over)) {
+          int32_t Fg = hl ? s_F32[lane * G + gs] : 0;
+          if (__any_sync(FULLMASK, hl && Fg + wl > Ml)) {
             const int32_t Tl = Ml - wl;
             uint32_t cost[WPL];
-#pragma unroll
+BFSIM_UNROLL_W
             for (int j = 0; j < WPL; ++j) cost[j] = 0;
-#pragma unroll
-            for (int h = 0; h < HR; ++h) {
+#pragma unroll 4
+            for (int h = 0; h <= H; ++h) {
               const int32_t T = __shfl_sync(FULLMASK, Tl, h);
-#pragma unroll
-              for (int j = 0; j < WPL; ++j) cost[j] += static_cast<uint32_t>(T > Fr[j][h] ? T : Fr[j][h]);
+BFSIM_UNROLL_W
+              for (int j = 0; j < WPL; ++j) {
+                const int32_t f = s_F32[h * G + ((lane + 32 * j) < G ? lane + 32 * j : 0)];
+                cost[j] += static_cast<uint32_t>(T > f ? T : f);
+              }
             }
             uint64_t best = ~0ull;
-#pragma unroll
+BFSIM_UNROLL_W
             for (int j = 0; j < WPL; ++j) {
               const int g = lane + 32 * j;
               const uint64_t key = (static_cast<uint64_t>(cost[j]) << 32) |
-                                   (static_cast<uint64_t>(static_cast<uint32_t>(Fr[j][0])) << gbits) |
+                                   (static_cast<uint64_t>(static_cast<uint32_t>(F0r[j])) << gbits) |
                                    static_cast<uint64_t>(g);
               if (g < G && cp[j] > 0 && key < best) best = key;
             }
             gs = static_cast<int>(wmin_u64(best) & gmask);
+            Fg = hl ? s_F32[lane * G + gs] : 0;
           }
-          const int own = gs & 31, jj = gs >> 5;
-          // the owner adds w_h to the chosen row (recomputing w_h, no per-item
-          // array) and publishes the row; lane h then raises M_h with it
-          if (lane == own) {
-#pragma unroll
+          // lane h adds w_h to the chosen row and raises M_h; the owner lane
+          // updates the worker's registers
+          if (hl) {
+            const int32_t v = Fg + wl;
+            s_F32[lane * G + gs] = v;
+            Ml = v > Ml ? v : Ml;
+          }
+          if (lane == (gs & 31)) {
+            const int jj = gs >> 5;
+BFSIM_UNROLL_W
             for (int j = 0; j < WPL; ++j)
               if (j == jj) {
-#pragma unroll
-                for (int h = 0; h < HR; ++h) {
-                  const int32_t dh = d32 * h;
-                  Fr[j][h] += h < limH ? c + (dh < sat ? dh : sat) : 0;
-                  if (h <= H) s_F32[h * G + gs] = Fr[j][h];
-                }
+                F0r[j] += c;
                 cp[j] -= 1;
                 A[j] += c + ak;
                 s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
                 adm[j] += 1;
-                if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
-                  int r = static_cast<int>((k + o - 1) % Hm);
-                  s_Wc[r * G + gs] += 1;
-                  s_Wa[r * G + gs] += c + ak;
-                }
               }
-          }
-          __syncwarp();
-          if (hl) {
-            const int32_t v = s_F32[lane * G + gs];
-            Ml = v > Ml ? v : Ml;
+            if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
+              int r = static_cast<int>((k + o - 1) % Hm);
+              s_Wc[r * G + gs] += 1;
+              s_Wa[r * G + gs] += c + ak;
+            }
           }
           __syncwarp();
         }
