@@ -134,6 +134,9 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
   if (lb >= 2147483647.0)
     return fail(err, errlen, BFSIM_EINVAL, "GPU path: per-worker load bound exceeds 2^31");
   if (in.max_decode >= (1 << 30)) return fail(err, errlen, BFSIM_EINVAL, "GPU path: decode too long");
+  // noisy draws are carried clamped to +-2^29, exact while decode lengths stay below 2^28
+  if (s.lookahead == BFSIM_LOOKAHEAD_NOISY && s.noise_sigma > 0.0 && in.max_decode >= (1 << 28))
+    return fail(err, errlen, BFSIM_EINVAL, "GPU path: decode too long for noisy lookahead");
   // per-slot a = s - drift*x is int32 (Poisson runs check this per step: BFSIM_ERANGE)
   if (s.mode == BFSIM_MODE_OVERLOADED &&
       static_cast<double>(d) * static_cast<double>(s.warmup + s.steps) + in.s_max >= 2147483647.0)
@@ -258,6 +261,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     // the draw pass's shared-memory atomics (int32 difference arrays over h)
     // and the register chain's [h][g] view mirror come first
     items.push_back({&p.o_mt, 312 * 8});
+    items.push_back({&p.o_nring, 2048 * 4});  // kRing draws
     items.push_back({&p.o_pre, (G + 1) * 4LL});
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 4});
@@ -482,8 +486,9 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
                                                     (228 * 1024) / per_sm - 2048));
     budget = std::max(budget, 8 * 1024);
     make_plan(g, scen_host, inputs_host, budget);
-    // one warp (trajectory) per CTA: latency-bound warps spread over every SM
-    g.wpc = 1;
+    // one warp (trajectory) per CTA: latency-bound warps spread over every SM;
+    // noisy: the trajectory's CTA has a second warp producing its draws
+    g.wpc = g.noisy ? 2 : 1;
     KParams probe{};
     probe.plan = g.plan;
     int occ = 0;
@@ -491,10 +496,10 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
                                        nullptr, &occ);
     if (rc != 0 || occ <= 0)
       return fail(err, errlen, BFSIM_ECUDA, "step kernel does not fit on the device");
-    int64_t warps_needed = static_cast<int64_t>(g.idx.size());
-    int64_t ctas = (warps_needed + g.wpc - 1) / g.wpc;
+    const int traj_per_cta = g.noisy ? 1 : g.wpc;
+    int64_t ctas = (static_cast<int64_t>(g.idx.size()) + traj_per_cta - 1) / traj_per_cta;
     g.grid = static_cast<int>(std::min<int64_t>(ctas, static_cast<int64_t>(occ) * ctx->sm_count));
-    ws_total += g.plan.ws_stride * g.grid * g.wpc;
+    ws_total += g.plan.ws_stride * g.grid * traj_per_cta;
     gl.push_back(&g);
   }
   for (auto* g : gl) order.insert(order.end(), g->idx.begin(), g->idx.end());
@@ -545,7 +550,7 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
       cudaStreamWaitEvent(us, ctx->join[gi % kMaxGroups], 0);
     }
     off += static_cast<int64_t>(g.idx.size());
-    ws_off += g.plan.ws_stride * g.grid * g.wpc;
+    ws_off += g.plan.ws_stride * g.grid * (g.noisy ? 1 : g.wpc);
   }
   cudaEventRecord(ctx->t1, us);
   ctx->timed = true;

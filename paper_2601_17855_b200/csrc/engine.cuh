@@ -41,6 +41,7 @@ struct Plan {
   // appended entries (o_eid), the admitted waiting draws, admitted-id bitmap
   // and its word prefix (cold)
   int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre, o_selb, o_eid, o_pre;
+  int64_t o_nring;  // noisy: the producer warp's ring of draws (kRing int32)
   // bfio-greedy with WPL >= 16: per-worker argmin keys
   int64_t o_key;
   // completion calendar (cal != 0, large G*B): list heads [R][32], per-slot links

@@ -160,6 +160,94 @@ __device__ __forceinline__ double mt_canonical(uint64_t u) {
   return r >= 1.0 ? 0x1.fffffffffffffp-1 : r;
 }
 
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Noisy lookahead draw stream (make_preview, policies.hpp:74-76). Every step
+// the reference draws normal_distribution(0, sigma) values from the
+// simulation's mt19937_64 -- one per active request, then one per waiting
+// request (engine.hpp:131, 204-231) -- with a fresh distribution object per
+// call, so draw i of the trajectory is the i-th accepted polar pair of the
+// engine stream (random.tcc:1809-1844), independent of how draws are split
+// into steps. A producer warp generates that stream ahead of the simulation
+// warp: lround(N(0, sigma)) of every accepted pair, clamped to +-2^29 (exact
+// for the previews: decode lengths are < 2^28), stored as 2 v + (near-tie
+// flag) in a shared-memory ring of kRing entries. ctr[0] = draws produced,
+// ctr[1] = draws the consumer has released, ctr[2] = trajectory finished.
+constexpr int kRing = 2048;
+
+// lround(y * sqrt(-2 ln r2 / r2) * sigma) for an accepted pair, and whether it
+// lies next to a half-integer (CUDA log is within 1 ulp of glibc's). A float
+// estimate decides it unless the value lies within 1e-5 (relative) of a
+// half-integer: its error is below 1e-6 relative (-ln r2 as -log1pf(r2 - 1),
+// r2 - 1 exact in double, or -logf(r2), each within 1 ulp and ~2.2 ulp after
+// the input rounding, then IEEE division, sqrt and products, no fast-math:
+// ~10 ulp of 2^-24 in all). Those rare draws take the reference's
+// double-precision formula, every step spelled with _rn (no FMA).
+__device__ __forceinline__ int normal_code(double y, double r2, double sigma, float sf) {
+  const float r2f = static_cast<float>(r2);
+  const float L = r2 < 0.25 ? -logf(r2f) : -log1pf(static_cast<float>(r2 - 1.0));
+  const float nf = static_cast<float>(y) * sqrtf(2.0f * L / r2f) * sf;
+  const float af = fabsf(nf);
+  long long l;
+  int tie = 0;
+  if (af < 1048576.0f && fabsf((af - floorf(af)) - 0.5f) > 1e-5f * fmaxf(1.0f, af)) {
+    l = static_cast<long long>(lroundf(nf));
+  } else {
+    const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
+    const double nv = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), sigma), 0.0);
+    l = llround(nv);
+    const double av = fabs(nv);
+    tie = fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av) ? 1 : 0;
+  }
+  l = l > (1ll << 29) ? (1ll << 29) : (l < -(1ll << 29) ? -(1ll << 29) : l);
+  return static_cast<int>(2 * l + tie);
+}
+
+static __device__ void noisy_producer(uint64_t* mt, int* ring, unsigned* ctr, uint64_t seed, double sigma) {
+  const int lane = threadIdx.x & 31;
+  const float sf = static_cast<float>(sigma);
+  mt_seed(mt, seed);  // Simulation::rng_(config.seed), engine.hpp:97-98
+  int mt_i = kMtN;
+  unsigned prod = 0;
+  for (;;) {
+    // room for one slice (<= 32 draws) behind the consumer's release
+    for (;;) {
+      const unsigned rel = ld_acquire(&ctr[1]);
+      if (static_cast<int>(prod - rel) <= kRing - 32) break;
+      if (ld_acquire(&ctr[2])) return;
+      __nanosleep(64);
+    }
+    if (ld_acquire(&ctr[2])) return;
+    if (mt_i >= kMtN) {
+      mt_twist(mt);
+      mt_i = 0;
+    }
+    const int np = (kMtN - mt_i) >> 1;  // pairs left in the block
+    const bool valid = lane < np;
+    const int pi = mt_i + 2 * (valid ? lane : 0);
+    const double u1 = mt_canonical(mt_temper(mt[pi]));
+    const double u2 = mt_canonical(mt_temper(mt[pi + 1]));
+    const double x = __dsub_rn(__dmul_rn(2.0, u1), 1.0);
+    const double y = __dsub_rn(__dmul_rn(2.0, u2), 1.0);
+    const double r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    const bool acc = valid && !(r2 > 1.0 || r2 == 0.0);
+    const unsigned am = __ballot_sync(FULLMASK, acc);
+    if (acc) ring[(prod + __popc(am & lanemask_lt())) & (kRing - 1)] = normal_code(y, r2, sigma, sf);
+    __threadfence_block();
+    __syncwarp();
+    prod += __popc(am);
+    mt_i += 2 * (np < 32 ? np : 32);
+    if (lane == 0) st_release(&ctr[0], prod);
+  }
+}
+
 // Array placement from the planner. SM: every code is a shared-memory offset,
 // so the compiler emits 32-bit shared loads/stores. Otherwise a code < 0 is
 // byte (-code - 1) of the warp's global workspace.
@@ -393,7 +481,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   // difference arrays over h in int32 (shared-memory atomics); per-item
   // draws; the admitted waiting draws and the admitted-id bitmap that gives
   // waiting ranks.
-  uint64_t* s_mt = NOISY ? at<SM, uint64_t>(sm, ws, pl.o_mt) : nullptr;
+  int* s_ring = NOISY ? at<SM, int>(sm, ws, pl.o_nring) : nullptr;  // the producer warp's draws
+  unsigned* s_ctr = NOISY ? at<SM, unsigned>(sm, ws, pl.o_misc) + 1 : nullptr;
   int2* s_E = NOISY ? gat<int2>(ws, pl.o_lst) : nullptr;
   int32_t* s_Eid = NOISY ? gat<int32_t>(ws, pl.o_eid) : nullptr;
   int32_t* s_pre = NOISY ? at<SM, int32_t>(sm, ws, pl.o_pre) : nullptr;
@@ -435,11 +524,10 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     for (int i = lane; i < pl.R * 32; i += 32) calh[i] = -1;
   if (cal == 2)
     for (int i = lane; i < kWheel * LS; i += 32) calh[i] = -1;
-  int mt_i = kMtN;       // next engine word in the current block (always even)
+  unsigned cons = 0;     // noisy: draws of the stream consumed so far
   long long aw0 = 0;     // first bitmap word holding a waiting (revealed, unadmitted) id
   bool ntie = false;     // a draw landed next to an lround tie (BFSIM_FLAG_NOISE_NEAR_TIE)
   if constexpr (NOISY) {
-    mt_seed(s_mt, sc.seed);  // Simulation::rng_(config.seed), engine.hpp:97-98
     for (long long w = lane; w < (N + 63) / 64 + 1; w += 32) abits[w] = 0ull;
     for (long long w = lane; w < (N + 31) / 32 + 1; w += 32) selb[w] = 0u;
   }
@@ -758,167 +846,74 @@ BFSIM_UNROLL_W
   // The D = active + waiting normal draws of one step, in the reference's
   // order (engine.hpp:131 with GCC's right-to-left argument evaluation:
   // worker_views -- g ascending, insertion order, engine.hpp:204-220 -- then
-  // waiting_views in waiting order, :222-231). Every polar attempt takes the
-  // two engine words at an even position, so lane l tests the pair at
-  // mt_i + 2l and accepted pairs are numbered by a ballot prefix. With
-  // `values`, active draw r (< act) goes straight into the lookahead views:
-  // it belongs to entry r - pre[g] of worker g's insertion-ordered list
-  // (s_pre: exclusive prefix of the active counts), whose {finish step, a}
-  // the lanes read coalesced (consecutive draws, consecutive entries), and
-  // the request's preview (make_preview, policies.hpp:67-90) is added to the
-  // worker's difference arrays over h with shared-memory atomics: w_i + d*h
-  // while h < min(c_i, rem_i), its last workload a + d*f while
-  // rem_i <= h < c_i, with c_i = min(max(1, rem_i + lround(n_i)), H + 1) and
-  // rem_i = f - k + 1. A waiting draw's value is kept (nzb[r]) only when its
-  // request is admitted this step.
+  // waiting_views in waiting order, :222-231), taken from the producer
+  // warp's ring (draws cons .. cons + D - 1 of the trajectory's stream).
+  // With `values`, active draw r (< act) goes straight into the lookahead
+  // views: it belongs to entry r - pre[g] of worker g's insertion-ordered
+  // list (s_pre: exclusive prefix of the active counts), whose
+  // {finish step, a} the lanes read coalesced (consecutive draws, consecutive
+  // entries), and the request's preview (make_preview, policies.hpp:67-90) is
+  // added to the worker's difference arrays over h with shared-memory
+  // atomics: w_i + d*h while h < min(c_i, rem_i), its last workload a + d*f
+  // while rem_i <= h < c_i, with c_i = min(max(1, rem_i + lround(n_i)), H + 1)
+  // and rem_i = f - k + 1. A waiting draw's value is kept (nzb[r]) only when
+  // its request is admitted this step.
   auto gen_normals = [&](long long D, bool values) {
-    long long got = 0;
-    int gq = 0;  // this lane's last worker (its draws only move forward)
-    while (got < D) {
-      if (mt_i >= kMtN) {
-        mt_twist(s_mt);
-        mt_i = 0;
-      }
-      // every remaining pair of the block at once: pair mt_i/2 + 32t + lane
-      const int np = (kMtN - mt_i) >> 1;
-      double yv[5], r2v[5];
-      unsigned am[5];
-      int before[5];
-      int run = 0;
-#pragma unroll
-      for (int t = 0; t < 5; ++t) {
-        const int pq = 32 * t + lane;
-        const bool valid = pq < np;
-        const int pi = mt_i + 2 * (valid ? pq : 0);
-        const double u1 = mt_canonical(mt_temper(s_mt[pi]));
-        const double u2 = mt_canonical(mt_temper(s_mt[pi + 1]));
-        const double x = __dsub_rn(__dmul_rn(2.0, u1), 1.0);
-        yv[t] = __dsub_rn(__dmul_rn(2.0, u2), 1.0);
-        r2v[t] = __dadd_rn(__dmul_rn(x, x), __dmul_rn(yv[t], yv[t]));
-        am[t] = __ballot_sync(FULLMASK, valid && !(r2v[t] > 1.0 || r2v[t] == 0.0));
-        before[t] = run;
-        run += __popc(am[t]);
-      }
-      if (values) {
-        // values are needed for every active request's draw and for the
-        // waiting draws of requests admitted this step; the rest of the
-        // waiting draws only advance the stream. The five slots of a lane are
-        // independent: every stage is issued for all of them before the next
-        // (loads in flight together, interleaved log / div / sqrt chains).
-        long long rr[5];
-        bool nd[5];
-        unsigned sw[5];
-#pragma unroll
-        for (int t = 0; t < 5; ++t) {
-          rr[t] = got + before[t] + __popc(am[t] & lanemask_lt());
-          nd[t] = ((am[t] >> lane) & 1u) && rr[t] < D;
-          const long long p = rr[t] - act;
-          sw[t] = (nd[t] && p >= 0) ? __ldcg(selb + (p >> 5)) : 0u;
+    if (values) {
+      int gq = 0;  // this lane's last worker (its draws only move forward)
+      for (long long r0 = 0; r0 < D; r0 += 32) {
+        const long long r = r0 + lane;
+        bool need = r < D;
+        if (need && r >= act) {
+          const long long p = r - act;
+          need = (__ldcg(selb + (p >> 5)) >> (p & 31)) & 1u;
         }
-        bool anyn = false;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) {
-          if (nd[t] && rr[t] >= act) nd[t] = (sw[t] >> ((rr[t] - act) & 31)) & 1u;
-          anyn = anyn || nd[t];
-        }
-        if (__any_sync(FULLMASK, anyn)) {
-          // lround(y * sqrt(-2 ln r2 / r2) * sigma) is an integer: a float
-          // estimate decides it unless the value lies within 1e-5 (relative)
-          // of a half-integer. The estimate's error is below 1e-6 relative:
-          // -ln r2 as -log1pf(r2 - 1) (r2 - 1 exact in double) or -logf(r2),
-          // each within 1 ulp and ~2.2 ulp after the input rounding, then
-          // IEEE division, sqrt and products (no fast-math): ~10 ulp of 2^-24
-          // in all. Those rare draws take the reference's double-precision
-          // formula (the previous, exact path).
-          const float sf = static_cast<float>(sigma);
-          long long lr[5];
-          bool ex[5];
-          bool anyex = false;
-#pragma unroll
-          for (int t = 0; t < 5; ++t) {
-            const float r2f = static_cast<float>(r2v[t]);
-            const float L = r2v[t] < 0.25 ? -logf(r2f) : -log1pf(static_cast<float>(r2v[t] - 1.0));
-            const float nf = static_cast<float>(yv[t]) * sqrtf(2.0f * L / r2f) * sf;
-            const float af = fabsf(nf);
-            ex[t] = nd[t] && (!(af < 1048576.0f) || fabsf((af - floorf(af)) - 0.5f) <= 1e-5f * fmaxf(1.0f, af));
-            lr[t] = nd[t] && !ex[t] ? static_cast<long long>(lroundf(nf)) : 0;
-            anyex = anyex || ex[t];
+        if (__any_sync(FULLMASK, need)) {
+          // everything before r0 is consumed: release it first (the producer
+          // may be waiting for room), then wait for this chunk's draws
+          if (lane == 0) st_release(&s_ctr[1], cons + static_cast<unsigned>(r0));
+          const unsigned hi = cons + static_cast<unsigned>(r0 + 32 < D ? r0 + 32 : D);
+          for (int spin = 0; static_cast<int>(ld_acquire(&s_ctr[0]) - hi) < 0; ++spin) {
+            if (spin > (1 << 26)) __trap();  // the producer never stalls this long: fail, do not hang
+            __nanosleep(32);
           }
-          if (__any_sync(FULLMASK, anyex)) {
-#pragma unroll
-            for (int t = 0; t < 5; ++t) {
-              if (!ex[t]) continue;
-              const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2v[t])), r2v[t]));
-              const double nv = __dadd_rn(__dmul_rn(__dmul_rn(yv[t], mult), sigma), 0.0);
-              const long long l = llround(nv);
-              lr[t] = l > (1ll << 30) ? (1ll << 30) : (l < -(1ll << 30) ? -(1ll << 30) : l);
-              // CUDA log is within 1 ulp of glibc's; only a draw this close
-              // to a half-integer could round differently
-              const double av = fabs(nv);
-              if (fabs(__dsub_rn(av, floor(av)) - 0.5) <= 1e-12 * fmax(1.0, av)) ntie = true;
-            }
-          }
-          int gt[5], pt[5];
-#pragma unroll
-          for (int t = 0; t < 5; ++t) {
-            gt[t] = gq;
-            pt[t] = 0;
-            if (nd[t] && rr[t] < act) {
+          if (need) {
+            const int code = s_ring[(cons + static_cast<unsigned>(r)) & (kRing - 1)];
+            const long long lr = code >> 1;
+            if (code & 1) ntie = true;
+            if (r >= act) {
+              nzb[r] = static_cast<int32_t>(lr);
+            } else {
               int g = gq, nx = s_pre[g + 1];
-              while (nx <= rr[t]) nx = s_pre[++g + 1];
+              while (nx <= r) nx = s_pre[++g + 1];
               gq = g;
-              gt[t] = g;
-              pt[t] = static_cast<int>(rr[t]) - s_pre[g];
+              const int2 e = s_E[g * B + static_cast<int>(r - s_pre[g])];
+              const long long f = static_cast<uint32_t>(e.x);
+              const long long a = e.y;
+              const long long rem = f - k + 1;
+              long long pred = rem + lr;
+              pred = pred > 1 ? pred : 1;
+              const long long c = pred < H + 1 ? pred : H + 1;
+              const long long m = c < rem ? c : rem;
+              if (m <= H) {
+                atomicAdd(&n_Wa[(m - 1) * G + g], static_cast<int32_t>(-(a + d * k)));
+                atomicAdd(&s_Wc[(m - 1) * G + g], -1);
+              }
+              if (c > rem) {
+                const int32_t wl = static_cast<int32_t>(a + d * f);
+                atomicAdd(&n_Wa[(rem - 1) * G + g], wl);
+                if (c <= H) atomicAdd(&n_Wa[(c - 1) * G + g], -wl);
+              }
             }
           }
-          int2 et[5];
-#pragma unroll
-          for (int t = 0; t < 5; ++t)
-            et[t] = (nd[t] && rr[t] < act) ? s_E[gt[t] * B + pt[t]] : make_int2(0, 0);
-#pragma unroll
-          for (int t = 0; t < 5; ++t) {
-            if (!nd[t]) continue;
-            if (rr[t] >= act) {
-              nzb[rr[t]] = static_cast<int32_t>(lr[t]);
-              continue;
-            }
-            const int g = gt[t];
-            const long long f = static_cast<uint32_t>(et[t].x);
-            const long long a = et[t].y;
-            const long long rem = f - k + 1;
-            long long pred = rem + lr[t];
-            pred = pred > 1 ? pred : 1;
-            const long long c = pred < H + 1 ? pred : H + 1;
-            const long long m = c < rem ? c : rem;
-            if (m <= H) {
-              atomicAdd(&n_Wa[(m - 1) * G + g], static_cast<int32_t>(-(a + d * k)));
-              atomicAdd(&s_Wc[(m - 1) * G + g], -1);
-            }
-            if (c > rem) {
-              const int32_t wl = static_cast<int32_t>(a + d * f);
-              atomicAdd(&n_Wa[(rem - 1) * G + g], wl);
-              if (c <= H) atomicAdd(&n_Wa[(c - 1) * G + g], -wl);
-            }
-          }
+          __syncwarp();
+          if (lane == 0) st_release(&s_ctr[1], hi);
         }
-      }
-      const long long need = D - got;
-      if (run >= need) {
-        int rest = static_cast<int>(need), used = 0;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) {
-          const int c = __popc(am[t]);
-          if (rest > 0 && rest <= c) used = 32 * t + static_cast<int>(__fns(am[t], 0, rest)) + 1;
-          rest -= c;
-        }
-        mt_i += 2 * used;
-        got = D;
-      } else {
-        mt_i = kMtN;
-        got += run;
       }
     }
+    cons += static_cast<unsigned>(D);
     __syncwarp();
+    if (lane == 0) st_release(&s_ctr[1], cons);
   };
 
   // Rank of each admitted request in the waiting order (arrival order of the
@@ -2047,6 +2042,7 @@ BFSIM_UNROLL_W
   }
   if (emit_steps && k > scap) flags |= BFSIM_FLAG_STEP_OVERFLOW;
   if (NOISY && __any_sync(FULLMASK, ntie)) flags |= BFSIM_FLAG_NOISE_NEAR_TIE;
+  if (NOISY && lane == 0) st_release(&s_ctr[2], 1u);  // the producer warp stops
   if (lane == 0) {
     bfsim_result_t r;
     r.status = status;
@@ -2081,27 +2077,56 @@ BFSIM_UNROLL_W
   __syncwarp();
 }
 
+// Noisy variants run two warps per trajectory (the simulation warp and the
+// draw producer), <= 144 registers a thread so 7 trajectories share an SM.
 template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) step_kernel(KParams P) {
+__global__ void __launch_bounds__(NOISY ? 64 : kWarpsPerCta * 32, NOISY ? 7 : 1) step_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int wpc = blockDim.x >> 5;
-  unsigned char* sm = smem + static_cast<size_t>(warp) * P.plan.smem_per_warp;
-  unsigned char* ws = P.ws + static_cast<size_t>(blockIdx.x * wpc + warp) * P.plan.ws_stride;
-  for (;;) {
-    int qi = 0;
-    if (lane == 0) qi = atomicAdd(P.queue, 1);
-    qi = __shfl_sync(FULLMASK, qi, 0);
-    if (qi >= P.n) break;
-    run_traj<MODE, POL, WPL, SMALLC, SM, NOISY, HR>(P, P.order[qi], sm, ws);
+  if constexpr (NOISY) {
+    // one trajectory per CTA: warp 0 simulates, warp 1 produces its draws
+    __shared__ int s_qi;
+    unsigned char* sm = smem;
+    unsigned char* ws = P.ws + static_cast<size_t>(blockIdx.x) * P.plan.ws_stride;
+    unsigned* ctr = at<SM, unsigned>(sm, ws, P.plan.o_misc) + 1;
+    for (;;) {
+      if (threadIdx.x == 0) {
+        s_qi = atomicAdd(P.queue, 1);
+        ctr[0] = ctr[1] = ctr[2] = 0u;
+      }
+      __syncthreads();
+      const int qi = s_qi;
+      if (qi >= P.n) break;
+      const int si = P.order[qi];
+      if (warp == 0) {
+        run_traj<MODE, POL, WPL, SMALLC, SM, NOISY, HR>(P, si, sm, ws);
+      } else {
+        const bfsim_scenario_t& sc = P.scen[si];
+        noisy_producer(at<SM, uint64_t>(sm, ws, P.plan.o_mt), at<SM, int>(sm, ws, P.plan.o_nring), ctr, sc.seed,
+                       sc.noise_sigma);
+      }
+      __syncthreads();
+    }
+  } else {
+    const int wpc = blockDim.x >> 5;
+    unsigned char* sm = smem + static_cast<size_t>(warp) * P.plan.smem_per_warp;
+    unsigned char* ws = P.ws + static_cast<size_t>(blockIdx.x * wpc + warp) * P.plan.ws_stride;
+    for (;;) {
+      int qi = 0;
+      if (lane == 0) qi = atomicAdd(P.queue, 1);
+      qi = __shfl_sync(FULLMASK, qi, 0);
+      if (qi >= P.n) break;
+      run_traj<MODE, POL, WPL, SMALLC, SM, NOISY, HR>(P, P.order[qi], sm, ws);
+    }
   }
 }
 
 template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
 int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
   auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM, NOISY, HR>;
-  size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * wpc;
+  // noisy: one trajectory (arena) per CTA of two warps
+  size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * (NOISY ? 1 : wpc);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
