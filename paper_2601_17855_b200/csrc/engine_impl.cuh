@@ -222,7 +222,7 @@ static __device__ void noisy_producer(uint64_t* mt, int* ring, unsigned* ctr, ui
       const unsigned rel = ld_acquire(&ctr[1]);
       if (static_cast<int>(prod - rel) <= kRing - 32) break;
       if (ld_acquire(&ctr[2])) return;
-      __nanosleep(64);
+      __nanosleep(256);  // the consumer is behind: stay off the issue slots
     }
     if (ld_acquire(&ctr[2])) return;
     if (mt_i >= kMtN) {
@@ -860,9 +860,24 @@ BFSIM_UNROLL_W
   // its request is admitted this step.
   auto gen_normals = [&](long long D, bool values) {
     if (values) {
-      int gq = 0;  // this lane's last worker (its draws only move forward)
+      // the list entry of this lane's next active draw is fetched one chunk
+      // ahead (worker search from the lane's last worker: draws only move
+      // forward)
+      int gq = 0, gn = 0;
+      int2 en = make_int2(0, 0);
+      auto fetch = [&](long long r) {
+        int g = gq, nx = s_pre[g + 1];
+        while (nx <= r) nx = s_pre[++g + 1];
+        gq = g;
+        gn = g;
+        en = s_E[g * B + static_cast<int>(r - s_pre[g])];
+      };
+      if (lane < act) fetch(lane);
       for (long long r0 = 0; r0 < D; r0 += 32) {
         const long long r = r0 + lane;
+        const int gc = gn;
+        const int2 ec = en;
+        if (r + 32 < act) fetch(r + 32);
         bool need = r < D;
         if (need && r >= act) {
           const long long p = r - act;
@@ -884,12 +899,9 @@ BFSIM_UNROLL_W
             if (r >= act) {
               nzb[r] = static_cast<int32_t>(lr);
             } else {
-              int g = gq, nx = s_pre[g + 1];
-              while (nx <= r) nx = s_pre[++g + 1];
-              gq = g;
-              const int2 e = s_E[g * B + static_cast<int>(r - s_pre[g])];
-              const long long f = static_cast<uint32_t>(e.x);
-              const long long a = e.y;
+              const int g = gc;
+              const long long f = static_cast<uint32_t>(ec.x);
+              const long long a = ec.y;
               const long long rem = f - k + 1;
               long long pred = rem + lr;
               pred = pred > 1 ? pred : 1;
@@ -1898,13 +1910,20 @@ BFSIM_UNROLL_W
             const int nold = __shfl_sync(FULLMASK, n[j], src);
             int2* Eg = s_E + g * B;
             int w = 0;
-            for (int p0 = 0; p0 < nold; p0 += 32) {
-              const int p = p0 + lane;
+            for (int p0 = 0; p0 < nold; p0 += 64) {  // two chunks in flight
+              const int p = p0 + lane, p2 = p0 + 32 + lane;
               const int2 e = p < nold ? Eg[p] : make_int2(0, 0);
+              const int2 e2 = p2 < nold ? Eg[p2] : make_int2(0, 0);
               const bool keep = p < nold && static_cast<uint32_t>(e.x) != kf;
+              const bool keep2 = p2 < nold && static_cast<uint32_t>(e2.x) != kf;
               const unsigned km = __ballot_sync(FULLMASK, keep);
+              const unsigned km2 = __ballot_sync(FULLMASK, keep2);
+              // in place: an entry moves only to a lower position, and the
+              // second chunk's reads are done before any store
               if (keep) Eg[w + __popc(km & lanemask_lt())] = e;
               w += __popc(km);
+              if (keep2) Eg[w + __popc(km2 & lanemask_lt())] = e2;
+              w += __popc(km2);
             }
           }
         }
