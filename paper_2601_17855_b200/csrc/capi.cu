@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
@@ -229,6 +230,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   struct Item {
     int64_t* code;
     int64_t bytes;
+    bool core;  // always in shared memory: the kernel addresses it with 32-bit shared loads
   };
   // completion calendar: a 64-bucket wheel in shared memory for small G*B,
   // exact finish-step buckets in the workspace once the slots outgrow it
@@ -239,40 +241,45 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   // the warp's global workspace and later, smaller ones may still fit):
   // per-step scalars and per-worker state, class records, argmin keys, the
   // accounting ring, then the per-slot arrays, then per-admission scratch.
+  // Core arrays (touched on every step's dependent chain, small) are always
+  // in shared memory -- the kernel addresses them with 32-bit shared loads
+  // even in its spilled variant (engine_impl.cuh: at<true>) -- then the rest.
   std::vector<Item> items = {
-      {&p.o_rdt, 32 * 8}, {&p.o_rcs, 32 * 8}, {&p.o_rmx, 32 * 4}, {&p.o_rac, 32 * 4},
-      {&p.o_misc, 16},    {&p.o_capb, G * 4LL}, {&p.o_asum, G * 8LL}, {&p.o_cap, G * 4LL},
+      {&p.o_rdt, 32 * 8, true}, {&p.o_rcs, 32 * 8, true}, {&p.o_rmx, 32 * 4, true}, {&p.o_rac, 32 * 4, true},
+      {&p.o_misc, 16, true},    {&p.o_capb, G * 4LL, true}, {&p.o_asum, G * 8LL, true}, {&p.o_cap, G * 4LL, true},
   };
   if (!greedy) {  // level tables of the FIFO policies
-    items.push_back({&p.o_lvT, lvl * 4});
-    items.push_back({&p.o_lvV, lvl * 4});
-    items.push_back({&p.o_lvK, lvl * 4});
-    items.push_back({&p.o_lvM, lvl * wpl * 4});
+    items.push_back({&p.o_lvT, lvl * 4, true});
+    items.push_back({&p.o_lvV, lvl * 4, true});
+    items.push_back({&p.o_lvK, lvl * 4, true});
+    items.push_back({&p.o_lvM, lvl * wpl * 4, true});
   }
   if (greedy || ovl) {
-    items.push_back({&p.o_cls, 5LL * (S + 2) * 4});  // int4 records + int32 starts
-    items.push_back({&p.o_bm, bm_words * 8});
-    items.push_back({&p.o_pbm, bm_words * 8});
+    const bool c = greedy && g.small;  // <= 64 classes (SMALLC)
+    items.push_back({&p.o_cls, 5LL * (S + 2) * 4, c});  // int4 records + int32 starts
+    items.push_back({&p.o_bm, bm_words * 8, c});
+    items.push_back({&p.o_pbm, bm_words * 8, c});
   }
-  if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8});
+  if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8, false});
   // M, T, w of the lookahead chain
-  if (greedy && H > 0) items.push_back({&p.o_M, std::max<int64_t>(3 * (H + 1) * 8LL, 128)});
+  if (greedy && H > 0) items.push_back({&p.o_M, std::max<int64_t>(3 * (H + 1) * 8LL, 128), true});
   if (g.noisy) {
-    // the draw pass's shared-memory atomics (int32 difference arrays over h)
-    // and the register chain's [h][g] view mirror come first
-    items.push_back({&p.o_mt, 312 * 8});
-    items.push_back({&p.o_nring, 2048 * 4});  // kRing draws
-    items.push_back({&p.o_pre, (G + 1) * 4LL});
-    items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
-    items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 4});
-    if (g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G});
+    // the draw ring, the draw pass's shared-memory atomics (int32 difference
+    // arrays over h) and the int32 chain's [h][g] views
+    items.push_back({&p.o_mt, 312 * 8, true});
+    items.push_back({&p.o_nring, 2048 * 4, true});  // kRing draws
+    items.push_back({&p.o_pre, (G + 1) * 4LL, true});
+    items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4, true});
+    items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 4, true});
+    if (g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
   }
+  if (greedy && H > 0 && !g.noisy && g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
   // per-slot state touched every step (retire)
   items.push_back({&p.o_f, ((GB + 3) & ~3LL) * 4});
   items.push_back({&p.o_a, GB * 4});
   items.push_back({&p.o_stk, GB * 2});
   if (greedy && H > 0 && !g.noisy) {
-    items.push_back({&p.o_F, (H + 1) * (g.hr ? 4LL : 8LL) * G});  // int32 mirror for the register chain
+    if (!g.hr) items.push_back({&p.o_F, (H + 1) * 8LL * G});
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 8});
   }
@@ -303,7 +310,13 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   g.hot_bytes = hot;
   int64_t sm_off = 0, ws_off = 0;
   int spilled = 0;
+  for (auto& it : items)
+    if (it.core) {
+      *it.code = sm_off;
+      sm_off += (it.bytes + 15) & ~15LL;
+    }
   for (auto& it : items) {
+    if (it.core) continue;
     int64_t b = (it.bytes + 15) & ~15LL;
     if (sm_off + b <= smem_budget) {
       *it.code = sm_off;
@@ -496,6 +509,12 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
                                        nullptr, &occ);
     if (rc != 0 || occ <= 0)
       return fail(err, errlen, BFSIM_ECUDA, "step kernel does not fit on the device");
+    if (std::getenv("BFSIM_DEBUG_PLAN"))
+      std::fprintf(stderr,
+                   "bfsim plan: mode %d policy %d wpl %d noisy %d hr %d: %zu trajectories, %d B smem/trajectory "
+                   "(all_smem %d), occupancy %d CTAs/SM of %d warps, ws %lld B/trajectory\n",
+                   g.mode, g.policy, g.wpl, g.noisy, g.hr, g.idx.size(), g.plan.smem_per_warp, g.plan.all_smem, occ,
+                   g.wpc, static_cast<long long>(g.plan.ws_stride));
     const int traj_per_cta = g.noisy ? 1 : g.wpc;
     int64_t ctas = (static_cast<int64_t>(g.idx.size()) + traj_per_cta - 1) / traj_per_cta;
     g.grid = static_cast<int>(std::min<int64_t>(ctas, static_cast<int64_t>(occ) * ctx->sm_count));

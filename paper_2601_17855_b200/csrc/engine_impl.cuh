@@ -430,35 +430,35 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* s_x = at<SM, int32_t>(sm, ws, pl.o_x);
   int32_t* s_id = at<SM, int32_t>(sm, ws, pl.o_id);
   uint16_t* s_stk = at<SM, uint16_t>(sm, ws, pl.o_stk);
-  int32_t* s_capb = at<SM, int32_t>(sm, ws, pl.o_capb);
-  unsigned long long* s_asum = at<SM, unsigned long long>(sm, ws, pl.o_asum);
-  int32_t* s_cap = at<SM, int32_t>(sm, ws, pl.o_cap);
+  int32_t* s_capb = at<true, int32_t>(sm, ws, pl.o_capb);  // core arrays: always shared memory
+  unsigned long long* s_asum = at<true, unsigned long long>(sm, ws, pl.o_asum);
+  int32_t* s_cap = at<true, int32_t>(sm, ws, pl.o_cap);
   uint32_t* r_l = at<SM, uint32_t>(sm, ws, pl.o_rl);
-  double* r_dt = at<SM, double>(sm, ws, pl.o_rdt);
-  double* r_cs = at<SM, double>(sm, ws, pl.o_rcs);
-  uint32_t* r_mx = at<SM, uint32_t>(sm, ws, pl.o_rmx);
-  int32_t* r_ac = at<SM, int32_t>(sm, ws, pl.o_rac);
+  double* r_dt = at<true, double>(sm, ws, pl.o_rdt);
+  double* r_cs = at<true, double>(sm, ws, pl.o_rcs);
+  uint32_t* r_mx = at<true, uint32_t>(sm, ws, pl.o_rmx);
+  int32_t* r_ac = at<true, int32_t>(sm, ws, pl.o_rac);
   double* ring = gat<double>(ws, pl.o_ring);  // cold: global workspace (L1/L2)
   const int Rm = pl.R - 1;
   // per-class record {front, back, picks this step, deque base} + chain start
-  int4* c_rec = at<SM, int4>(sm, ws, pl.o_cls);
+  int4* c_rec = at<SM || (GREEDY && SMALLC), int4>(sm, ws, pl.o_cls);
   int32_t* c_cs = reinterpret_cast<int32_t*>(c_rec + (pl.S + 2));
   int2* deq = gat<int2>(ws, pl.o_deq);
   int2* stage = at<SM, int2>(sm, ws, pl.o_stage);  // prefetched (id|s, o) records
   int32_t* p_cl = at<SM, int32_t>(sm, ws, pl.o_pcl);
   int32_t* p_t = at<SM, int32_t>(sm, ws, pl.o_pt);
   uint32_t* s_res = at<SM, uint32_t>(sm, ws, pl.o_res);
-  int32_t* lvT = at<SM, int32_t>(sm, ws, pl.o_lvT);
-  int32_t* lvV = at<SM, int32_t>(sm, ws, pl.o_lvV);
-  int32_t* lvK = at<SM, int32_t>(sm, ws, pl.o_lvK);
-  uint32_t* lvM = at<SM, uint32_t>(sm, ws, pl.o_lvM);
-  long long* s_F = at<SM, long long>(sm, ws, pl.o_F);
-  long long* s_M = at<SM, long long>(sm, ws, pl.o_M);
-  int32_t* s_Wc = at<SM, int32_t>(sm, ws, pl.o_Wc);
-  long long* s_Wa = at<SM, long long>(sm, ws, pl.o_Wa);
+  int32_t* lvT = at<SM || !GREEDY, int32_t>(sm, ws, pl.o_lvT);
+  int32_t* lvV = at<SM || !GREEDY, int32_t>(sm, ws, pl.o_lvV);
+  int32_t* lvK = at<SM || !GREEDY, int32_t>(sm, ws, pl.o_lvK);
+  uint32_t* lvM = at<SM || !GREEDY, uint32_t>(sm, ws, pl.o_lvM);
+  long long* s_F = at<SM || (HR > 0), long long>(sm, ws, pl.o_F);
+  long long* s_M = at<SM || GREEDY, long long>(sm, ws, pl.o_M);
+  int32_t* s_Wc = at<SM || NOISY, int32_t>(sm, ws, pl.o_Wc);
+  long long* s_Wa = at<SM || NOISY, long long>(sm, ws, pl.o_Wa);
   int32_t* o_c = at<SM, int32_t>(sm, ws, pl.o_oc);
   int2* cbuf = gat<int2>(ws, pl.o_cbuf);  // cold: completions (x, finish step) for TPOT
-  int32_t* s_misc = at<SM, int32_t>(sm, ws, pl.o_misc);  // [0] completion-buffer fill
+  int32_t* s_misc = at<true, int32_t>(sm, ws, pl.o_misc);  // [0] completion-buffer fill
   int32_t* o_o = at<SM, int32_t>(sm, ws, pl.o_oo);
   int32_t* o_id = at<SM, int32_t>(sm, ws, pl.o_oid);
   uint64_t* s_key = (GREEDY && WPL >= 16) ? at<SM, uint64_t>(sm, ws, pl.o_key) : nullptr;
@@ -481,11 +481,11 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   // difference arrays over h in int32 (shared-memory atomics); per-item
   // draws; the admitted waiting draws and the admitted-id bitmap that gives
   // waiting ranks.
-  int* s_ring = NOISY ? at<SM, int>(sm, ws, pl.o_nring) : nullptr;  // the producer warp's draws
-  unsigned* s_ctr = NOISY ? at<SM, unsigned>(sm, ws, pl.o_misc) + 1 : nullptr;
+  int* s_ring = NOISY ? at<true, int>(sm, ws, pl.o_nring) : nullptr;  // the producer warp's draws
+  unsigned* s_ctr = NOISY ? at<true, unsigned>(sm, ws, pl.o_misc) + 1 : nullptr;
   int2* s_E = NOISY ? gat<int2>(ws, pl.o_lst) : nullptr;
   int32_t* s_Eid = NOISY ? gat<int32_t>(ws, pl.o_eid) : nullptr;
-  int32_t* s_pre = NOISY ? at<SM, int32_t>(sm, ws, pl.o_pre) : nullptr;
+  int32_t* s_pre = NOISY ? at<true, int32_t>(sm, ws, pl.o_pre) : nullptr;
   int32_t* n_Wa = NOISY ? reinterpret_cast<int32_t*>(s_Wa) : nullptr;
   int32_t* o_nz = NOISY ? at<SM, int32_t>(sm, ws, pl.o_onz) : nullptr;
   int32_t* nzb = NOISY ? gat<int32_t>(ws, pl.o_nzb) : nullptr;
@@ -515,8 +515,8 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
     }
   ClassSet<SMALLC> wset, pset;  // waiting classes; classes picked in phase 1
   {
-    uint64_t* bm = at<SM, uint64_t>(sm, ws, pl.o_bm);
-    uint64_t* pbm = at<SM, uint64_t>(sm, ws, pl.o_pbm);
+    uint64_t* bm = at<SM || (GREEDY && SMALLC), uint64_t>(sm, ws, pl.o_bm);
+    uint64_t* pbm = at<SM || (GREEDY && SMALLC), uint64_t>(sm, ws, pl.o_pbm);
     wset.init(bm, bm + 64, S);
     pset.init(pbm, pbm + 64, S);
   }
@@ -2108,7 +2108,7 @@ __global__ void __launch_bounds__(NOISY ? 64 : kWarpsPerCta * 32, NOISY ? 7 : 1)
     __shared__ int s_qi;
     unsigned char* sm = smem;
     unsigned char* ws = P.ws + static_cast<size_t>(blockIdx.x) * P.plan.ws_stride;
-    unsigned* ctr = at<SM, unsigned>(sm, ws, P.plan.o_misc) + 1;
+    unsigned* ctr = at<true, unsigned>(sm, ws, P.plan.o_misc) + 1;
     for (;;) {
       if (threadIdx.x == 0) {
         s_qi = atomicAdd(P.queue, 1);
@@ -2122,7 +2122,7 @@ __global__ void __launch_bounds__(NOISY ? 64 : kWarpsPerCta * 32, NOISY ? 7 : 1)
         run_traj<MODE, POL, WPL, SMALLC, SM, NOISY, HR>(P, si, sm, ws);
       } else {
         const bfsim_scenario_t& sc = P.scen[si];
-        noisy_producer(at<SM, uint64_t>(sm, ws, P.plan.o_mt), at<SM, int>(sm, ws, P.plan.o_nring), ctr, sc.seed,
+        noisy_producer(at<true, uint64_t>(sm, ws, P.plan.o_mt), at<true, int>(sm, ws, P.plan.o_nring), ctr, sc.seed,
                        sc.noise_sigma);
       }
       __syncthreads();
