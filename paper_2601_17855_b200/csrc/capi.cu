@@ -274,6 +274,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     if (g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
   }
   if (greedy && H > 0 && !g.noisy && g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
+  if (greedy && H > 0 && g.hr) items.push_back({&p.o_admc, G * 4LL, true});
   // per-slot state touched every step (retire)
   items.push_back({&p.o_f, ((GB + 3) & ~3LL) * 4});
   items.push_back({&p.o_a, GB * 4});

@@ -42,6 +42,7 @@ struct Plan {
   // and its word prefix (cold)
   int64_t o_mt, o_lst, o_onz, o_nzb, o_abits, o_zpre, o_selb, o_eid, o_pre;
   int64_t o_nring;  // noisy: the producer warp's ring of draws (kRing int32)
+  int64_t o_admc;   // per-worker admissions of the step (int32 chain)
   // bfio-greedy with WPL >= 16: per-worker argmin keys
   int64_t o_key;
   // completion calendar (cal != 0, large G*B): list heads [R][32], per-slot links

@@ -432,6 +432,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   uint16_t* s_stk = at<SM, uint16_t>(sm, ws, pl.o_stk);
   int32_t* s_capb = at<true, int32_t>(sm, ws, pl.o_capb);  // core arrays: always shared memory
   unsigned long long* s_asum = at<true, unsigned long long>(sm, ws, pl.o_asum);
+  int32_t* s_admc = at<true, int32_t>(sm, ws, pl.o_admc);  // admissions per worker (int32 chain)
   int32_t* s_cap = at<true, int32_t>(sm, ws, pl.o_cap);
   uint32_t* r_l = at<SM, uint32_t>(sm, ws, pl.o_rl);
   double* r_dt = at<true, double>(sm, ws, pl.o_rdt);
@@ -1554,9 +1555,15 @@ BFSIM_UNROLL_W
             const int32_t v = s_F32[lane * G + g];
             Ml = v > Ml ? v : Ml;
           }
-        int32_t F0r[WPL];
+        // The chain's per-worker state is in shared memory too (lane-owned
+        // registers would be spilled at this kernel's register budget): the
+        // free slots left (s_cap, already the pre-admission cap), the
+        // admissions so far (s_admc, rank of the next one) and the workload
+        // admitted (s_asum), folded into the registers after the chain.
 BFSIM_UNROLL_W
-        for (int j = 0; j < WPL; ++j) F0r[j] = lane + 32 * j < G ? s_F32[lane + 32 * j] : 0;
+        for (int j = 0; j < WPL; ++j)
+          if (lane + 32 * j < G) s_admc[lane + 32 * j] = 0;
+        __syncwarp();
         const int32_t d32 = static_cast<int32_t>(d);
         const int32_t dl = d32 * lane;
         for (int q = 0; q < U; ++q) {
@@ -1572,11 +1579,15 @@ BFSIM_UNROLL_W
           // and the smallest (F_0, g) tie-break key, so it wins outright.
           // Otherwise the full scan over every worker.
           key_t fk = KMAX;
+          int32_t F0v[WPL];
+          bool fre[WPL];
 BFSIM_UNROLL_W
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
-            const key_t kk = (static_cast<key_t>(static_cast<uint32_t>(F0r[j])) << gbits) | static_cast<key_t>(g);
-            if (g < G && cp[j] > 0 && kk < fk) fk = kk;
+            F0v[j] = g < G ? s_F32[g] : 0;
+            fre[j] = g < G && s_cap[g] > 0;
+            const key_t kk = (static_cast<key_t>(static_cast<uint32_t>(F0v[j])) << gbits) | static_cast<key_t>(g);
+            if (fre[j] && kk < fk) fk = kk;
           }
           int gs = static_cast<int>(wmin(fk) & static_cast<key_t>(gmask));
           int32_t Fg = hl ? s_F32[lane * G + gs] : 0;
@@ -1599,31 +1610,26 @@ BFSIM_UNROLL_W
             for (int j = 0; j < WPL; ++j) {
               const int g = lane + 32 * j;
               const uint64_t key = (static_cast<uint64_t>(cost[j]) << 32) |
-                                   (static_cast<uint64_t>(static_cast<uint32_t>(F0r[j])) << gbits) |
+                                   (static_cast<uint64_t>(static_cast<uint32_t>(F0v[j])) << gbits) |
                                    static_cast<uint64_t>(g);
-              if (g < G && cp[j] > 0 && key < best) best = key;
+              if (fre[j] && key < best) best = key;
             }
             gs = static_cast<int>(wmin_u64(best) & gmask);
             Fg = hl ? s_F32[lane * G + gs] : 0;
           }
-          // lane h adds w_h to the chosen row and raises M_h; the owner lane
-          // updates the worker's registers
+          // lane h adds w_h to the chosen row (row 0: its F_0) and raises
+          // M_h; the owner lane books the admission
           if (hl) {
             const int32_t v = Fg + wl;
             s_F32[lane * G + gs] = v;
             Ml = v > Ml ? v : Ml;
           }
           if (lane == (gs & 31)) {
-            const int jj = gs >> 5;
-BFSIM_UNROLL_W
-            for (int j = 0; j < WPL; ++j)
-              if (j == jj) {
-                F0r[j] += c;
-                cp[j] -= 1;
-                A[j] += c + ak;
-                s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(adm[j]) << 16);
-                adm[j] += 1;
-              }
+            const int rank = s_admc[gs];
+            s_admc[gs] = rank + 1;
+            s_cap[gs] -= 1;
+            s_asum[gs] += static_cast<unsigned long long>(static_cast<long long>(c) + ak);
+            s_res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(rank) << 16);
             if (!NOISY && o <= H) {  // finishes inside the window [k, k+H-1]
               int r = static_cast<int>((k + o - 1) % Hm);
               s_Wc[r * G + gs] += 1;
@@ -1631,6 +1637,15 @@ BFSIM_UNROLL_W
             }
           }
           __syncwarp();
+        }
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j) {
+          const int g = lane + 32 * j;
+          if (g >= G) continue;
+          adm[j] = s_admc[g];
+          cp[j] = s_cap[g];
+          A[j] += static_cast<long long>(s_asum[g]);
+          s_asum[g] = 0;
         }
         __syncwarp();
       } else {
