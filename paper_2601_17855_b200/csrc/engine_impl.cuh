@@ -1594,14 +1594,15 @@ BFSIM_UNROLL_W
           if (__any_sync(FULLMASK, hl && Fg + wl > Ml)) {
             const int32_t Tl = Ml - wl;
             uint32_t cost[WPL];
+            const int32_t* col = s_F32 + (lane < G ? lane : 0);  // this lane's column, row h at h * G
 BFSIM_UNROLL_W
             for (int j = 0; j < WPL; ++j) cost[j] = 0;
 #pragma unroll 4
-            for (int h = 0; h <= H; ++h) {
+            for (int h = 0; h <= H; ++h, col += G) {
               const int32_t T = __shfl_sync(FULLMASK, Tl, h);
 BFSIM_UNROLL_W
               for (int j = 0; j < WPL; ++j) {
-                const int32_t f = s_F32[h * G + ((lane + 32 * j) < G ? lane + 32 * j : 0)];
+                const int32_t f = lane + 32 * j < G ? col[32 * j] : 0;
                 cost[j] += static_cast<uint32_t>(T > f ? T : f);
               }
             }
