@@ -177,6 +177,17 @@ int reg_chain_width(const bfsim_scenario_t& s, const bfsim_input_t& in) {
   return s.horizon < 8 ? 8 : 24;
 }
 
+// Placement-chain kind of a scenario: the int32 register-budget chain (8, 24:
+// H < chain, G <= 128), the wide CTA (1: bfio-greedy with a window on
+// G > 128, not noisy; ceil(G / 128) warps share the chain) or the
+// single-warp shared-memory chain (0).
+int chain_kind(const bfsim_scenario_t& s, const bfsim_input_t& in, int noisy) {
+  const int hr = reg_chain_width(s, in);
+  if (hr) return hr;
+  if (s.policy == BFSIM_POLICY_BFIO_GREEDY && s.horizon > 0 && !noisy && s.workers > 128) return 1;
+  return 0;
+}
+
 int wpl_for(int G) {
   int w = (G + 31) / 32;
   int p = 1;
@@ -273,6 +284,7 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 4, true});
     if (g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
   }
+  // int32 views (register-budget and wide chains)
   if (greedy && H > 0 && !g.noisy && g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
   if (greedy && H > 0 && g.hr) items.push_back({&p.o_admc, G * 4LL, true});
   // per-slot state touched every step (retire)
@@ -466,7 +478,7 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
     int small = in.s_max <= 64 ? 1 : 0;
     int wpl = wpl_for(s.workers);
     int noisy = noisy_variant(s);
-    int hr = reg_chain_width(s, in);
+    int hr = chain_kind(s, in, noisy);
     auto key = std::make_tuple(s.mode, s.policy, wpl, small, noisy, hr);
     auto& g = groups[key];
     g.mode = s.mode;
@@ -501,8 +513,9 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
     budget = std::max(budget, 8 * 1024);
     make_plan(g, scen_host, inputs_host, budget);
     // one warp (trajectory) per CTA: latency-bound warps spread over every SM;
-    // noisy: the trajectory's CTA has a second warp producing its draws
-    g.wpc = g.noisy ? 2 : 1;
+    // noisy: the trajectory's CTA has a second warp producing its draws;
+    // wide: ceil(G / 128) warps share the placement chain
+    g.wpc = g.noisy ? 2 : (g.hr == 1 ? std::max(1, g.wpl / 4) : 1);
     KParams probe{};
     probe.plan = g.plan;
     int occ = 0;
@@ -516,7 +529,7 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
                    "(all_smem %d), occupancy %d CTAs/SM of %d warps, ws %lld B/trajectory\n",
                    g.mode, g.policy, g.wpl, g.noisy, g.hr, g.idx.size(), g.plan.smem_per_warp, g.plan.all_smem, occ,
                    g.wpc, static_cast<long long>(g.plan.ws_stride));
-    const int traj_per_cta = g.noisy ? 1 : g.wpc;
+    const int traj_per_cta = (g.noisy || g.hr == 1) ? 1 : g.wpc;
     int64_t ctas = (static_cast<int64_t>(g.idx.size()) + traj_per_cta - 1) / traj_per_cta;
     g.grid = static_cast<int>(std::min<int64_t>(ctas, static_cast<int64_t>(occ) * ctx->sm_count));
     ws_total += g.plan.ws_stride * g.grid * traj_per_cta;
@@ -570,7 +583,7 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
       cudaStreamWaitEvent(us, ctx->join[gi % kMaxGroups], 0);
     }
     off += static_cast<int64_t>(g.idx.size());
-    ws_off += g.plan.ws_stride * g.grid * (g.noisy ? 1 : g.wpc);
+    ws_off += g.plan.ws_stride * g.grid * ((g.noisy || g.hr == 1) ? 1 : g.wpc);
   }
   cudaEventRecord(ctx->t1, us);
   ctx->timed = true;

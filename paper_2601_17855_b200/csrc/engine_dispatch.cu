@@ -17,6 +17,11 @@ int launch_step_kernel(int mode, int policy, int wpl, int small_classes, int noi
       return ovl ? launch_overloaded_jsq(wpl, hr, kp, grid, wpc, s, occupancy)
                  : launch_poisson_jsq(wpl, hr, kp, grid, wpc, s, occupancy);
     case BFSIM_POLICY_BFIO_GREEDY:
+      if (hr == 1)  // wide trajectories (G > 128 with a lookahead window): a CTA of wpc warps each
+        return ovl ? (small_classes ? launch_overloaded_greedy_wide_small(wpl, kp, grid, wpc, s, occupancy)
+                                    : launch_overloaded_greedy_wide_large(wpl, kp, grid, wpc, s, occupancy))
+                   : (small_classes ? launch_poisson_greedy_wide_small(wpl, kp, grid, wpc, s, occupancy)
+                                    : launch_poisson_greedy_wide_large(wpl, kp, grid, wpc, s, occupancy));
       if (ovl)
         return small_classes ? launch_overloaded_greedy_small(wpl, hr, kp, grid, wpc, s, occupancy)
                              : launch_overloaded_greedy_large(wpl, hr, kp, grid, wpc, s, occupancy);

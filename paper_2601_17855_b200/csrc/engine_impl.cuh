@@ -388,8 +388,162 @@ struct ClassSet<false> {
 
 // ---------------------------------------------------------------------------
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
-__device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned char* ws) {
+
+// ---------------------------------------------------------------------------
+// Wide trajectories (bfio-greedy with a lookahead window on G > 128 workers,
+// BASELINE C4's G = 256..1024; SURVEY hard part 3): the trajectory's CTA has
+// W = ceil(G / 128) warps. Warp 0 runs the step loop; for the placement chain
+// (phase 2, policies.hpp:339-367) it hands the items to all W warps, which
+// split the workers (thread t: workers t, t + 32 W, ...; at most 4 each).
+// The views F_h[g] and maxima M_h are int32 rows in shared memory (every load
+// is below 2^31: validate_scenario); costs are summed in 64 bits.
+struct WideChain {
+  int cmd;  // 1: run the chain below, 0: the trajectory is done
+  int U, H, G, gbits, Hm, trunc;
+  long long k, d, ak;
+  const int32_t* o_c;
+  const int32_t* o_o;
+  int32_t* F;   // [h][g]
+  int32_t* M;   // [h]
+  int32_t* cap;
+  int32_t* admc;
+  unsigned long long* asum;
+  uint32_t* res;
+  int32_t* Wc;
+  long long* Wa;
+};
+
+// Named barrier 1 over the CTA's nthreads (warp-converged first: bar.sync is
+// the .aligned form).
+__device__ __forceinline__ void cta_bar(int nthreads) {
+  __syncwarp();
+  asm volatile("barrier.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Per item: the fast-path candidate g* = argmin (F_0[g], g) over free
+// workers (per-warp minima exchanged in shared memory); when no horizon of
+// g* would rise above the current maximum it wins outright (its cost is the
+// minimum sum_h M_h and its tie-break key the smallest). Otherwise every
+// thread scores its workers, cost = sum_h max(M_h - w_h, F_h[g]) (the
+// reference's sum_h max(M_h, F_h[g] + w_h) less sum_h w_h, which does not
+// depend on g: same argmin and ties over (cost, F_0, g)), and the per-warp
+// best (cost, F_0, g) are exchanged again. Threads over h then add w_h to the
+// chosen row and raise M_h; the owner books the admission.
+static __device__ void wide_chain(const WideChain& wsh, unsigned long long (*red)[2], int nthreads) {
+  // a private copy: once the chain's last barrier is passed, warp 0 may
+  // already be writing the next chain's parameters
+  const WideChain w = wsh;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = nthreads >> 5;
+  const int G = w.G, H = w.H, gbits = w.gbits;
+  const long long d = w.d;
+  int32_t* F = w.F;
+  int32_t* M = w.M;
+  const uint64_t gmask = (1ull << gbits) - 1ull;
+  for (int h = warp; h <= H; h += nw) {  // M_h = max over every worker
+    int32_t m = 0;
+    for (int g = lane; g < G; g += 32) m = F[h * G + g] > m ? F[h * G + g] : m;
+    m = static_cast<int32_t>(__reduce_max_sync(FULLMASK, static_cast<uint32_t>(m)));
+    if (lane == 0) M[h] = m;
+  }
+  cta_bar(nthreads);
+  for (int q = 0; q < w.U; ++q) {
+    const int c = w.o_c[q], o = w.o_o[q];
+    const long long lim = (w.trunc && o < H + 1) ? H + 1 : o;
+    const int limH = static_cast<int>(lim < H + 1 ? lim : H + 1);
+    const long long sat = d * (o - 1);
+    uint64_t fk = ~0ull;
+    for (int g = t; g < G; g += nthreads)
+      if (w.cap[g] > 0) {
+        const uint64_t kk = (static_cast<uint64_t>(static_cast<uint32_t>(F[g])) << gbits) | static_cast<uint64_t>(g);
+        fk = kk < fk ? kk : fk;
+      }
+    fk = wmin_u64(fk);
+    if (lane == 0) red[warp][0] = fk;
+    cta_bar(nthreads);
+    uint64_t best = ~0ull;
+    for (int i = 0; i < nw; ++i) best = red[i][0] < best ? red[i][0] : best;
+    int gs = static_cast<int>(best & gmask);
+    // thread t checks (and below updates) horizons t, t + nthreads, ...: no
+    // thread reads a row entry another thread writes in this item
+    bool over = false;
+    for (int h = t; h <= H; h += nthreads) {
+      const long long wh = h < limH ? c + (d * h < sat ? d * h : sat) : 0;
+      over = over || F[h * G + gs] + wh > M[h];
+    }
+    const unsigned ow = __ballot_sync(FULLMASK, over);
+    if (lane == 0) red[warp][1] = ow;
+    cta_bar(nthreads);
+    unsigned long long anyo = 0;
+    for (int i = 0; i < nw; ++i) anyo |= red[i][1];
+    if (anyo) {  // the same outcome in every warp
+      long long cost[4] = {0, 0, 0, 0};
+      for (int h = 0; h <= H; ++h) {
+        const long long wh = h < limH ? c + (d * h < sat ? d * h : sat) : 0;
+        const long long T = M[h] - wh;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int g = t + j * nthreads;
+          if (g < G) {
+            const long long f = F[h * G + g];
+            cost[j] += T > f ? T : f;
+          }
+        }
+      }
+      uint64_t bc = ~0ull, bk = ~0ull;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int g = t + j * nthreads;
+        if (g < G && w.cap[g] > 0) {
+          const uint64_t c64 = static_cast<uint64_t>(cost[j]);
+          const uint64_t k2 = (static_cast<uint64_t>(static_cast<uint32_t>(F[g])) << gbits) | static_cast<uint64_t>(g);
+          if (c64 < bc || (c64 == bc && k2 < bk)) {
+            bc = c64;
+            bk = k2;
+          }
+        }
+      }
+      const uint64_t cmin = wmin_u64(bc);
+      const uint64_t kmin = wmin_u64(bc == cmin ? bk : ~0ull);
+      cta_bar(nthreads);  // every thread has read red[][] above
+      if (lane == 0) {
+        red[warp][0] = cmin;
+        red[warp][1] = kmin;
+      }
+      cta_bar(nthreads);
+      uint64_t c2 = ~0ull, k2 = ~0ull;
+      for (int i = 0; i < nw; ++i)
+        if (red[i][0] < c2 || (red[i][0] == c2 && red[i][1] < k2)) {
+          c2 = red[i][0];
+          k2 = red[i][1];
+        }
+      gs = static_cast<int>(k2 & gmask);
+    }
+    for (int h = t; h <= H; h += nthreads) {
+      const long long wh = h < limH ? c + (d * h < sat ? d * h : sat) : 0;
+      const int32_t v = static_cast<int32_t>(F[h * G + gs] + wh);
+      F[h * G + gs] = v;
+      if (v > M[h]) M[h] = v;
+    }
+    if (t == gs % nthreads) {
+      const int rank = w.admc[gs];
+      w.admc[gs] = rank + 1;
+      w.cap[gs] -= 1;
+      w.asum[gs] += static_cast<unsigned long long>(c + w.ak);
+      w.res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(rank) << 16);
+      if (o <= H) {  // finishes inside the window [k, k+H-1]
+        const int r = static_cast<int>((w.k + o - 1) % w.Hm);
+        w.Wc[r * G + gs] += 1;
+        w.Wa[r * G + gs] += c + w.ak;
+      }
+    }
+    cta_bar(nthreads);
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR, bool WIDE = false>
+__device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned char* ws, WideChain* wctl = nullptr,
+                         unsigned long long (*wred)[2] = nullptr) {
   constexpr bool OVL = MODE == BFSIM_MODE_OVERLOADED;
   constexpr bool GREEDY = POL == BFSIM_POLICY_BFIO_GREEDY;
   static_assert(!NOISY || (GREEDY && !OVL), "noisy lookahead: Poisson bfio-greedy only");
@@ -453,7 +607,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* lvV = at<SM || !GREEDY, int32_t>(sm, ws, pl.o_lvV);
   int32_t* lvK = at<SM || !GREEDY, int32_t>(sm, ws, pl.o_lvK);
   uint32_t* lvM = at<SM || !GREEDY, uint32_t>(sm, ws, pl.o_lvM);
-  long long* s_F = at<SM || (HR > 0), long long>(sm, ws, pl.o_F);
+  long long* s_F = at<SM || (HR > 0) || WIDE, long long>(sm, ws, pl.o_F);
   long long* s_M = at<SM || GREEDY, long long>(sm, ws, pl.o_M);
   int32_t* s_Wc = at<SM || NOISY, int32_t>(sm, ws, pl.o_Wc);
   long long* s_Wa = at<SM || NOISY, long long>(sm, ws, pl.o_Wa);
@@ -1426,7 +1580,7 @@ BFSIM_UNROLL_W
       // (HR > 0: int32 views F_h[g] in shared memory, row-major [h][g], for
       // the chain below)
       int32_t* s_F32 = reinterpret_cast<int32_t*>(s_F);
-      if constexpr (!NOISY && HR > 0) {
+      if constexpr (!NOISY && (HR > 0 || WIDE)) {
 BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           const int g = lane + 32 * j;
@@ -1446,7 +1600,7 @@ BFSIM_UNROLL_W
           }
         }
       }
-      if constexpr (!NOISY && HR == 0) {
+      if constexpr (!NOISY && HR == 0 && !WIDE) {
 BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           int g = lane + 32 * j;
@@ -1639,6 +1793,50 @@ BFSIM_UNROLL_W
           }
           __syncwarp();
         }
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j) {
+          const int g = lane + 32 * j;
+          if (g >= G) continue;
+          adm[j] = s_admc[g];
+          cp[j] = s_cap[g];
+          A[j] += static_cast<long long>(s_asum[g]);
+          s_asum[g] = 0;
+        }
+        __syncwarp();
+      } else if constexpr (WIDE) {
+        // the CTA's W warps place the items together (wide_chain); the
+        // per-worker chain state goes through shared memory and is folded
+        // into warp 0's registers afterwards
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j)
+          if (lane + 32 * j < G) s_admc[lane + 32 * j] = 0;
+        if (lane == 0) {
+          WideChain& w = *wctl;
+          w.cmd = 1;
+          w.U = U;
+          w.H = H;
+          w.G = G;
+          w.gbits = gbits;
+          w.Hm = Hm;
+          w.trunc = trunc ? 1 : 0;
+          w.k = k;
+          w.d = d;
+          w.ak = ak;
+          w.o_c = o_c;
+          w.o_o = o_o;
+          w.F = reinterpret_cast<int32_t*>(s_F);
+          w.M = reinterpret_cast<int32_t*>(s_M);
+          w.cap = s_cap;
+          w.admc = s_admc;
+          w.asum = s_asum;
+          w.res = s_res;
+          w.Wc = s_Wc;
+          w.Wa = s_Wa;
+        }
+        __threadfence_block();
+        const int nthreads = static_cast<int>(blockDim.x);
+        cta_bar(nthreads);  // the helper warps start
+        wide_chain(*wctl, wred, nthreads);
 BFSIM_UNROLL_W
         for (int j = 0; j < WPL; ++j) {
           const int g = lane + 32 * j;
@@ -2114,12 +2312,40 @@ BFSIM_UNROLL_W
 
 // Noisy variants run two warps per trajectory (the simulation warp and the
 // draw producer), <= 144 registers a thread so 7 trajectories share an SM.
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
-__global__ void __launch_bounds__(NOISY ? 64 : kWarpsPerCta * 32, NOISY ? 7 : 1) step_kernel(KParams P) {
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR, bool WIDE = false>
+__global__ void __launch_bounds__(NOISY ? 64 : (WIDE ? 256 : kWarpsPerCta * 32), NOISY ? 7 : 1) step_kernel(KParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if constexpr (NOISY) {
+  if constexpr (WIDE) {
+    // one trajectory per CTA: warp 0 simulates, the other warps join its
+    // placement chains (wide_chain)
+    __shared__ int s_qi;
+    __shared__ WideChain s_w;
+    __shared__ unsigned long long s_red[8][2];
+    unsigned char* sm = smem;
+    unsigned char* ws = P.ws + static_cast<size_t>(blockIdx.x) * P.plan.ws_stride;
+    const int nthreads = static_cast<int>(blockDim.x);
+    for (;;) {
+      if (threadIdx.x == 0) s_qi = atomicAdd(P.queue, 1);
+      __syncthreads();
+      const int qi = s_qi;
+      if (qi >= P.n) break;
+      if (warp == 0) {
+        run_traj<MODE, POL, WPL, SMALLC, SM, NOISY, HR, WIDE>(P, P.order[qi], sm, ws, &s_w, s_red);
+        if (lane == 0) s_w.cmd = 0;
+        __threadfence_block();
+        cta_bar(nthreads);  // the helper warps leave
+      } else {
+        for (;;) {
+          cta_bar(nthreads);
+          if (s_w.cmd == 0) break;
+          wide_chain(s_w, s_red, nthreads);
+        }
+      }
+      __syncthreads();
+    }
+  } else if constexpr (NOISY) {
     // one trajectory per CTA: warp 0 simulates, warp 1 produces its draws
     __shared__ int s_qi;
     unsigned char* sm = smem;
@@ -2157,11 +2383,11 @@ __global__ void __launch_bounds__(NOISY ? 64 : kWarpsPerCta * 32, NOISY ? 7 : 1)
   }
 }
 
-template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR>
+template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR, bool WIDE = false>
 int launch_t(const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
-  auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM, NOISY, HR>;
-  // noisy: one trajectory (arena) per CTA of two warps
-  size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * (NOISY ? 1 : wpc);
+  auto fn = step_kernel<MODE, POL, WPL, SMALLC, SM, NOISY, HR, WIDE>;
+  // noisy / wide: one trajectory (arena) per CTA of several warps
+  size_t smem = static_cast<size_t>(kp.plan.smem_per_warp) * ((NOISY || WIDE) ? 1 : wpc);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return static_cast<int>(e);
@@ -2197,6 +2423,24 @@ int launch_w(int wpl, int hr, const KParams& kp, int grid, int wpc, cudaStream_t
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
+// Wide trajectories (G > 128, bfio-greedy with a window, not noisy): own units.
+template <int MODE, int POL, bool SMALLC>
+int launch_wide(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) {
+  const bool sm = kp.plan.all_smem != 0;
+  switch (wpl) {
+    case 8:
+      return sm ? launch_t<MODE, POL, 8, SMALLC, true, false, 0, true>(kp, grid, wpc, s, occ)
+                : launch_t<MODE, POL, 8, SMALLC, false, false, 0, true>(kp, grid, wpc, s, occ);
+    case 16:
+      return sm ? launch_t<MODE, POL, 16, SMALLC, true, false, 0, true>(kp, grid, wpc, s, occ)
+                : launch_t<MODE, POL, 16, SMALLC, false, false, 0, true>(kp, grid, wpc, s, occ);
+    case 32:
+      return sm ? launch_t<MODE, POL, 32, SMALLC, true, false, 0, true>(kp, grid, wpc, s, occ)
+                : launch_t<MODE, POL, 32, SMALLC, false, false, 0, true>(kp, grid, wpc, s, occ);
+  }
+  return static_cast<int>(cudaErrorInvalidValue);
+}
+
 // One instantiation unit per (mode, policy, class-set kind, noisy): both
 // arena placements (all-shared / spilled) and every workers-per-lane width.
 template <int MODE, int POL, bool SMALLC, bool NOISY>
@@ -2225,5 +2469,15 @@ BFSIM_DECLARE_UNIT(launch_overloaded_fcfs)
 BFSIM_DECLARE_UNIT(launch_overloaded_jsq)
 BFSIM_DECLARE_UNIT(launch_overloaded_greedy_small)
 BFSIM_DECLARE_UNIT(launch_overloaded_greedy_large)
+#define BFSIM_DECLARE_WIDE_UNIT(NAME) \
+  int NAME(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ);
+#define BFSIM_DEFINE_WIDE_UNIT(NAME, M, SMALLC)                                         \
+  int NAME(int wpl, const KParams& kp, int grid, int wpc, cudaStream_t s, int* occ) { \
+    return detail::launch_wide<M, BFSIM_POLICY_BFIO_GREEDY, SMALLC>(wpl, kp, grid, wpc, s, occ); \
+  }
+BFSIM_DECLARE_WIDE_UNIT(launch_poisson_greedy_wide_small)
+BFSIM_DECLARE_WIDE_UNIT(launch_poisson_greedy_wide_large)
+BFSIM_DECLARE_WIDE_UNIT(launch_overloaded_greedy_wide_small)
+BFSIM_DECLARE_WIDE_UNIT(launch_overloaded_greedy_wide_large)
 
 }  // namespace bfsim
