@@ -401,17 +401,18 @@ struct WideChain {
   int cmd;  // 1: run the chain below, 0: the trajectory is done
   int U, H, G, gbits, Hm, trunc;
   long long k, d, ak;
+  // byte offsets of core arrays in the CTA's dynamic shared memory (the
+  // trajectory's arena starts at 0): views F [h][g] (int32), maxima M and
+  // per-item T_h = M_h - w_h (int32), free slots, admissions, admitted workload
+  int F, M, cap, admc, asum;
   const int32_t* o_c;
   const int32_t* o_o;
-  int32_t* F;   // [h][g]
-  int32_t* M;   // [h]
-  int32_t* cap;
-  int32_t* admc;
-  unsigned long long* asum;
   uint32_t* res;
   int32_t* Wc;
   long long* Wa;
 };
+
+extern __shared__ __align__(16) unsigned char bfsim_dsmem[];
 
 // Named barrier 1 over the CTA's nthreads (warp-converged first: bar.sync is
 // the .aligned form).
@@ -429,15 +430,20 @@ __device__ __forceinline__ void cta_bar(int nthreads) {
 // depend on g: same argmin and ties over (cost, F_0, g)), and the per-warp
 // best (cost, F_0, g) are exchanged again. Threads over h then add w_h to the
 // chosen row and raise M_h; the owner books the admission.
-static __device__ void wide_chain(const WideChain& wsh, unsigned long long (*red)[2], int nthreads) {
+static __device__ __forceinline__ void wide_chain(const WideChain& wsh, unsigned long long (*red)[2], int nthreads) {
   // a private copy: once the chain's last barrier is passed, warp 0 may
   // already be writing the next chain's parameters
   const WideChain w = wsh;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = nthreads >> 5;
   const int G = w.G, H = w.H, gbits = w.gbits;
   const long long d = w.d;
-  int32_t* F = w.F;
-  int32_t* M = w.M;
+  // core arrays addressed in the shared window (32-bit shared loads)
+  int32_t* F = reinterpret_cast<int32_t*>(bfsim_dsmem + w.F);
+  int32_t* M = reinterpret_cast<int32_t*>(bfsim_dsmem + w.M);
+  int32_t* Tsh = M + (H + 1);
+  int32_t* cap = reinterpret_cast<int32_t*>(bfsim_dsmem + w.cap);
+  int32_t* admc = reinterpret_cast<int32_t*>(bfsim_dsmem + w.admc);
+  unsigned long long* asum = reinterpret_cast<unsigned long long*>(bfsim_dsmem + w.asum);
   const uint64_t gmask = (1ull << gbits) - 1ull;
   for (int h = warp; h <= H; h += nw) {  // M_h = max over every worker
     int32_t m = 0;
@@ -453,7 +459,7 @@ static __device__ void wide_chain(const WideChain& wsh, unsigned long long (*red
     const long long sat = d * (o - 1);
     uint64_t fk = ~0ull;
     for (int g = t; g < G; g += nthreads)
-      if (w.cap[g] > 0) {
+      if (cap[g] > 0) {
         const uint64_t kk = (static_cast<uint64_t>(static_cast<uint32_t>(F[g])) << gbits) | static_cast<uint64_t>(g);
         fk = kk < fk ? kk : fk;
       }
@@ -469,6 +475,7 @@ static __device__ void wide_chain(const WideChain& wsh, unsigned long long (*red
     for (int h = t; h <= H; h += nthreads) {
       const long long wh = h < limH ? c + (d * h < sat ? d * h : sat) : 0;
       over = over || F[h * G + gs] + wh > M[h];
+      Tsh[h] = static_cast<int32_t>(M[h] - wh);  // for the full scan
     }
     const unsigned ow = __ballot_sync(FULLMASK, over);
     if (lane == 0) red[warp][1] = ow;
@@ -477,23 +484,21 @@ static __device__ void wide_chain(const WideChain& wsh, unsigned long long (*red
     for (int i = 0; i < nw; ++i) anyo |= red[i][1];
     if (anyo) {  // the same outcome in every warp
       long long cost[4] = {0, 0, 0, 0};
-      for (int h = 0; h <= H; ++h) {
-        const long long wh = h < limH ? c + (d * h < sat ? d * h : sat) : 0;
-        const long long T = M[h] - wh;
+      const int32_t* col = F + t;
+      for (int h = 0; h <= H; ++h, col += G) {
+        const int32_t T = Tsh[h];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int g = t + j * nthreads;
-          if (g < G) {
-            const long long f = F[h * G + g];
+        for (int j = 0; j < 4; ++j)
+          if (t + j * nthreads < G) {
+            const int32_t f = col[j * nthreads];
             cost[j] += T > f ? T : f;
           }
-        }
       }
       uint64_t bc = ~0ull, bk = ~0ull;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int g = t + j * nthreads;
-        if (g < G && w.cap[g] > 0) {
+        if (g < G && cap[g] > 0) {
           const uint64_t c64 = static_cast<uint64_t>(cost[j]);
           const uint64_t k2 = (static_cast<uint64_t>(static_cast<uint32_t>(F[g])) << gbits) | static_cast<uint64_t>(g);
           if (c64 < bc || (c64 == bc && k2 < bk)) {
@@ -525,10 +530,10 @@ static __device__ void wide_chain(const WideChain& wsh, unsigned long long (*red
       if (v > M[h]) M[h] = v;
     }
     if (t == gs % nthreads) {
-      const int rank = w.admc[gs];
-      w.admc[gs] = rank + 1;
-      w.cap[gs] -= 1;
-      w.asum[gs] += static_cast<unsigned long long>(c + w.ak);
+      const int rank = admc[gs];
+      admc[gs] = rank + 1;
+      cap[gs] -= 1;
+      asum[gs] += static_cast<unsigned long long>(c + w.ak);
       w.res[q] = static_cast<uint32_t>(gs) | (static_cast<uint32_t>(rank) << 16);
       if (o <= H) {  // finishes inside the window [k, k+H-1]
         const int r = static_cast<int>((w.k + o - 1) % w.Hm);
@@ -1824,11 +1829,11 @@ BFSIM_UNROLL_W
           w.ak = ak;
           w.o_c = o_c;
           w.o_o = o_o;
-          w.F = reinterpret_cast<int32_t*>(s_F);
-          w.M = reinterpret_cast<int32_t*>(s_M);
-          w.cap = s_cap;
-          w.admc = s_admc;
-          w.asum = s_asum;
+          w.F = static_cast<int>(pl.o_F);  // core arrays: offsets in the arena (at the start of
+          w.M = static_cast<int>(pl.o_M);  // the CTA's dynamic shared memory)
+          w.cap = static_cast<int>(pl.o_cap);
+          w.admc = static_cast<int>(pl.o_admc);
+          w.asum = static_cast<int>(pl.o_asum);
           w.res = s_res;
           w.Wc = s_Wc;
           w.Wa = s_Wa;
@@ -2314,7 +2319,7 @@ BFSIM_UNROLL_W
 // draw producer), <= 144 registers a thread so 7 trajectories share an SM.
 template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR, bool WIDE = false>
 __global__ void __launch_bounds__(NOISY ? 64 : (WIDE ? 256 : kWarpsPerCta * 32), NOISY ? 7 : 1) step_kernel(KParams P) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* smem = bfsim_dsmem;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if constexpr (WIDE) {
