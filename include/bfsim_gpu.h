@@ -195,6 +195,25 @@ int bfsim_sample_instance(int prefill_kind, int s_max, int decode_kind, double p
  * (oracle.hpp:177-183). Policy-independent; only the number consumed varies. */
 int bfsim_sample_stream(int prefill_kind, int s_max, int decode_kind, double p, int64_t fixed_o,
                         uint64_t seed, int64_t n, bfsim_sample_t* out, char* err, size_t errlen);
+/* Any PrefillDistribution / DecodeDistribution (workload.hpp:87-215), including
+ * the Empirical kinds (:109-118, :185-193):
+ *   prefill kind 0 uniform(fixed = s_max), 1 fixed_value(fixed), 2 empirical(values)
+ *   decode  kind 0 geometric(p), 1 fixed_length(fixed), 2 empirical(values)
+ * An empirical draw is values[uniform_int_distribution<size_t>(0, n_values - 1)(rng)];
+ * validation and messages follow the reference's factories. */
+typedef struct bfsim_dist_t {
+  int32_t kind;
+  int32_t reserved;
+  int64_t fixed;         /* uniform s_max / fixed value */
+  double p;              /* geometric success probability */
+  const int64_t* values; /* empirical list (kind 2) */
+  int64_t n_values;
+} bfsim_dist_t;
+int bfsim_sample_instance_dist(const bfsim_dist_t* prefill, const bfsim_dist_t* decode, double rate,
+                               double duration, uint64_t seed, bfsim_request_t* out, int64_t capacity,
+                               int64_t* n_out, char* err, size_t errlen);
+int bfsim_sample_stream_dist(const bfsim_dist_t* prefill, const bfsim_dist_t* decode, uint64_t seed, int64_t n,
+                             bfsim_sample_t* out, char* err, size_t errlen);
 /* Input statistics + class_base for a trace (records) or stream (samples).
  * class_base must hold s_max + 2 entries; call with class_base == NULL to learn s_max. */
 int bfsim_prepare_trace(const bfsim_request_t* rec, int64_t n, bfsim_input_t* info,

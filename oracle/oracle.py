@@ -155,6 +155,7 @@ class RefLib:
         self.lib = C.CDLL(path)
         L = self.lib
         L.ref_sample_instance.argtypes = [C.c_int, C.c_int, C.c_int, _f64, _i64, _f64, _f64, _u64, _vp, _i64, _vp, _vp, C.c_size_t]
+        L.ref_set_empirical.argtypes = [_vp, _i64, _vp, _i64]
         L.ref_run_poisson.argtypes = [_vp, _vp, _i64, _vp, _vp, C.c_size_t]
         L.ref_run_poisson.restype = _vp
         L.ref_run_overloaded.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _f64, _i64, _vp, _vp, C.c_size_t]
@@ -178,6 +179,12 @@ class RefLib:
         L.ref_bench_poisson.restype = _f64
         L.ref_bench_overloaded.argtypes = [_vp, _i64, C.c_int, C.c_int, C.c_int, _f64, _i64, C.c_int, _vp]
         L.ref_bench_overloaded.restype = _f64
+
+    def set_empirical(self, prefill_values, decode_values):
+        """Lists for the kind-2 (Empirical) distributions of the calls below."""
+        self._pv = np.ascontiguousarray(prefill_values, np.int64)
+        self._dv = np.ascontiguousarray(decode_values, np.int64)
+        self.lib.ref_set_empirical(abi.ptr(self._pv), self._pv.shape[0], abi.ptr(self._dv), self._dv.shape[0])
 
     def sample_instance(self, s_max=64, p=0.02, rate=50.0, duration=10.0, seed=0,
                         prefill_kind=0, decode_kind=0, fixed_o=1):

@@ -54,11 +54,18 @@ int code_of(const std::exception_ptr& ep, char* err, size_t errlen) {
   }
 }
 
+// kind 2: the reference's Empirical distributions over the lists set by
+// ref_set_empirical (test infrastructure: one list pair per process)
+std::vector<int> g_emp_prefill;
+std::vector<long> g_emp_decode;
+
 bfsim::PrefillDistribution make_prefill(int kind, int s_max) {
+  if (kind == 2) return bfsim::PrefillDistribution::empirical(g_emp_prefill);
   return kind == 1 ? bfsim::PrefillDistribution::fixed_value(s_max)
                    : bfsim::PrefillDistribution::uniform(s_max);
 }
 bfsim::DecodeDistribution make_decode(int kind, double p, long fixed_o) {
+  if (kind == 2) return bfsim::DecodeDistribution::empirical(g_emp_decode);
   return kind == 1 ? bfsim::DecodeDistribution::fixed_length(fixed_o)
                    : bfsim::DecodeDistribution::geometric(p);
 }
@@ -108,6 +115,11 @@ struct Handle {
 }  // namespace
 
 extern "C" {
+
+void ref_set_empirical(const int64_t* prefill, int64_t n_prefill, const int64_t* decode, int64_t n_decode) {
+  g_emp_prefill.assign(prefill, prefill + n_prefill);
+  g_emp_decode.assign(decode, decode + n_decode);
+}
 
 int ref_sample_instance(int prefill_kind, int s_max, int decode_kind, double p, int64_t fixed_o,
                         double rate, double duration, uint64_t seed, bfsim_request_t* out,

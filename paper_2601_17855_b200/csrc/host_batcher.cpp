@@ -19,21 +19,31 @@
 
 namespace {
 
-// PrefillDistribution::sample (workload.hpp:120-128) for the Uniform / Fixed kinds.
+// PrefillDistribution::sample (workload.hpp:120-128): Uniform, Fixed, Empirical.
 struct Prefill {
   int kind, s_max;
+  const int64_t* values = nullptr;
+  int64_t n_values = 0;
   int sample(std::mt19937_64& rng) const {
     if (kind == 1) return s_max;
+    if (kind == 2)
+      return static_cast<int>(values[std::uniform_int_distribution<std::size_t>(
+          0, static_cast<std::size_t>(n_values) - 1)(rng)]);
     return std::uniform_int_distribution<int>(1, s_max)(rng);
   }
 };
-// DecodeDistribution::sample (workload.hpp:195-204) for the Geometric / Fixed kinds.
+// DecodeDistribution::sample (workload.hpp:195-204): Geometric, Fixed, Empirical.
 struct Decode {
   int kind;
   double p;
   int64_t fixed;
+  const int64_t* values = nullptr;
+  int64_t n_values = 0;
   long sample(std::mt19937_64& rng) const {
     if (kind == 1) return static_cast<long>(fixed);
+    if (kind == 2)
+      return static_cast<long>(values[std::uniform_int_distribution<std::size_t>(
+          0, static_cast<std::size_t>(n_values) - 1)(rng)]);
     return 1 + std::geometric_distribution<long>(p)(rng);
   }
 };
@@ -54,6 +64,90 @@ int check_dists(int prefill_kind, int s_max, int decode_kind, double p, int64_t 
     return bfsim::fail(err, errlen, BFSIM_EINVAL, "decode: fixed length must be >= 1");
   if (decode_kind != 0 && decode_kind != 1)
     return bfsim::fail(err, errlen, BFSIM_EINVAL, "decode: unknown distribution kind");
+  return BFSIM_OK;
+}
+
+// Descriptor -> sampler, validated as the reference's factories do
+// (PrefillDistribution::empirical workload.hpp:109-118, DecodeDistribution::
+// empirical :185-193: empty list, value < 1).
+int make_dists(const bfsim_dist_t* pd, const bfsim_dist_t* dd, Prefill* pf, Decode* dc, char* err, size_t errlen) {
+  if (!pd || !dd) return bfsim::fail(err, errlen, BFSIM_EINVAL, "null distribution");
+  if (pd->kind == 2) {
+    if (!pd->values || pd->n_values < 1)
+      return bfsim::fail(err, errlen, BFSIM_EINVAL, "prefill: empty empirical list");
+    int64_t mx = 0;
+    for (int64_t i = 0; i < pd->n_values; ++i) {
+      if (pd->values[i] < 1) return bfsim::fail(err, errlen, BFSIM_EINVAL, "prefill: empirical value < 1");
+      if (pd->values[i] > BFSIM_MAX_CLASSES)
+        return bfsim::fail(err, errlen, BFSIM_EINVAL, "prefill: empirical value exceeds the GPU class limit");
+      mx = std::max(mx, pd->values[i]);
+    }
+    *pf = Prefill{2, static_cast<int>(mx), pd->values, pd->n_values};
+  } else {
+    if (pd->fixed > std::numeric_limits<int>::max())
+      return bfsim::fail(err, errlen, BFSIM_EINVAL, "prefill: value exceeds int");
+    int rc = check_dists(pd->kind, static_cast<int>(pd->fixed), 0, 0.5, 1, err, errlen);
+    if (rc) return rc;
+    *pf = Prefill{pd->kind, static_cast<int>(pd->fixed)};
+  }
+  if (dd->kind == 2) {
+    if (!dd->values || dd->n_values < 1)
+      return bfsim::fail(err, errlen, BFSIM_EINVAL, "decode: empty empirical list");
+    for (int64_t i = 0; i < dd->n_values; ++i) {
+      if (dd->values[i] < 1) return bfsim::fail(err, errlen, BFSIM_EINVAL, "decode: empirical value < 1");
+      if (dd->values[i] > std::numeric_limits<int32_t>::max())
+        return bfsim::fail(err, errlen, BFSIM_EINVAL, "decode: empirical value exceeds int32");
+    }
+    *dc = Decode{2, 0.0, 0, dd->values, dd->n_values};
+  } else {
+    int rc = check_dists(0, 1, dd->kind, dd->p, dd->fixed, err, errlen);
+    if (rc) return rc;
+    *dc = Decode{dd->kind, dd->p, dd->fixed};
+  }
+  return BFSIM_OK;
+}
+
+// sample_instance, workload.hpp:241-266: exponential gaps, then prefill, then
+// decode per arrival, all from one mt19937_64(seed).
+int sample_instance_impl(const Prefill& pf, const Decode& dc, double rate, double duration, uint64_t seed,
+                         bfsim_request_t* out, int64_t capacity, int64_t* n_out, char* err, size_t errlen) {
+  if (rate <= 0.0) return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_instance: rate must be > 0");
+  if (duration <= 0.0)
+    return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_instance: duration must be > 0");
+  std::mt19937_64 rng(seed);
+  std::exponential_distribution<double> gap(rate);
+  double t = gap(rng);
+  int64_t n = 0;
+  while (t < duration) {
+    int s = pf.sample(rng);
+    long o = dc.sample(rng);
+    if (o > std::numeric_limits<int32_t>::max())
+      return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_instance: decode exceeds int32");
+    if (out && n < capacity) {
+      out[n].arrival_time = t;
+      out[n].prefill = s;
+      out[n].decode = static_cast<int32_t>(o);
+    }
+    ++n;
+    t += gap(rng);
+  }
+  *n_out = n;
+  return BFSIM_OK;
+}
+
+// run_overloaded's top-up draws prefill then decode per pending request
+// (oracle.hpp:177-183) from mt19937_64(seed), independent of the policy.
+int sample_stream_impl(const Prefill& pf, const Decode& dc, uint64_t seed, int64_t n, bfsim_sample_t* out,
+                       char* err, size_t errlen) {
+  std::mt19937_64 rng(seed);
+  for (int64_t i = 0; i < n; ++i) {
+    int s = pf.sample(rng);
+    long o = dc.sample(rng);
+    if (o > std::numeric_limits<int32_t>::max())
+      return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_stream: decode exceeds int32");
+    out[i].prefill = s;
+    out[i].decode = static_cast<int32_t>(o);
+  }
   return BFSIM_OK;
 }
 
@@ -99,52 +193,34 @@ int bfsim_sample_instance(int prefill_kind, int s_max, int decode_kind, double p
                           int64_t capacity, int64_t* n_out, char* err, size_t errlen) {
   int rc = check_dists(prefill_kind, s_max, decode_kind, p, fixed_o, err, errlen);
   if (rc) return rc;
-  // sample_instance, workload.hpp:241-266: exponential gaps, then prefill, then
-  // decode per arrival, all from one mt19937_64(seed).
-  if (rate <= 0.0) return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_instance: rate must be > 0");
-  if (duration <= 0.0)
-    return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_instance: duration must be > 0");
-  Prefill pf{prefill_kind, s_max};
-  Decode dc{decode_kind, p, fixed_o};
-  std::mt19937_64 rng(seed);
-  std::exponential_distribution<double> gap(rate);
-  double t = gap(rng);
-  int64_t n = 0;
-  while (t < duration) {
-    int s = pf.sample(rng);
-    long o = dc.sample(rng);
-    if (o > std::numeric_limits<int32_t>::max())
-      return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_instance: decode exceeds int32");
-    if (out && n < capacity) {
-      out[n].arrival_time = t;
-      out[n].prefill = s;
-      out[n].decode = static_cast<int32_t>(o);
-    }
-    ++n;
-    t += gap(rng);
-  }
-  *n_out = n;
-  return BFSIM_OK;
+  return sample_instance_impl(Prefill{prefill_kind, s_max}, Decode{decode_kind, p, fixed_o}, rate, duration, seed,
+                              out, capacity, n_out, err, errlen);
+}
+
+int bfsim_sample_instance_dist(const bfsim_dist_t* prefill, const bfsim_dist_t* decode, double rate,
+                               double duration, uint64_t seed, bfsim_request_t* out, int64_t capacity,
+                               int64_t* n_out, char* err, size_t errlen) {
+  Prefill pf{0, 1};
+  Decode dc{0, 0.5, 1};
+  int rc = make_dists(prefill, decode, &pf, &dc, err, errlen);
+  if (rc) return rc;
+  return sample_instance_impl(pf, dc, rate, duration, seed, out, capacity, n_out, err, errlen);
 }
 
 int bfsim_sample_stream(int prefill_kind, int s_max, int decode_kind, double p, int64_t fixed_o,
                         uint64_t seed, int64_t n, bfsim_sample_t* out, char* err, size_t errlen) {
   int rc = check_dists(prefill_kind, s_max, decode_kind, p, fixed_o, err, errlen);
   if (rc) return rc;
-  // run_overloaded's top-up draws prefill then decode per pending request
-  // (oracle.hpp:177-183) from mt19937_64(seed), independent of the policy.
-  Prefill pf{prefill_kind, s_max};
-  Decode dc{decode_kind, p, fixed_o};
-  std::mt19937_64 rng(seed);
-  for (int64_t i = 0; i < n; ++i) {
-    int s = pf.sample(rng);
-    long o = dc.sample(rng);
-    if (o > std::numeric_limits<int32_t>::max())
-      return bfsim::fail(err, errlen, BFSIM_EINVAL, "sample_stream: decode exceeds int32");
-    out[i].prefill = s;
-    out[i].decode = static_cast<int32_t>(o);
-  }
-  return BFSIM_OK;
+  return sample_stream_impl(Prefill{prefill_kind, s_max}, Decode{decode_kind, p, fixed_o}, seed, n, out, err, errlen);
+}
+
+int bfsim_sample_stream_dist(const bfsim_dist_t* prefill, const bfsim_dist_t* decode, uint64_t seed, int64_t n,
+                             bfsim_sample_t* out, char* err, size_t errlen) {
+  Prefill pf{0, 1};
+  Decode dc{0, 0.5, 1};
+  int rc = make_dists(prefill, decode, &pf, &dc, err, errlen);
+  if (rc) return rc;
+  return sample_stream_impl(pf, dc, seed, n, out, err, errlen);
 }
 
 int bfsim_prepare_trace(const bfsim_request_t* rec, int64_t n, bfsim_input_t* info,

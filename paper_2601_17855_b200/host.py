@@ -56,6 +56,8 @@ def lib():
     L.bfsim_ctx_destroy.argtypes = [_vp]
     L.bfsim_sample_instance.argtypes = [C.c_int, C.c_int, C.c_int, _f64, _i64, _f64, _f64, _u64, _vp, _i64, _vp, _vp, _sz]
     L.bfsim_sample_stream.argtypes = [C.c_int, C.c_int, C.c_int, _f64, _i64, _u64, _i64, _vp, _vp, _sz]
+    L.bfsim_sample_instance_dist.argtypes = [_vp, _vp, _f64, _f64, _u64, _vp, _i64, _vp, _vp, _sz]
+    L.bfsim_sample_stream_dist.argtypes = [_vp, _vp, _u64, _i64, _vp, _vp, _sz]
     L.bfsim_prepare_trace.argtypes = [_vp, _i64, _vp, _vp, _vp, _sz]
     L.bfsim_prepare_stream.argtypes = [_vp, _i64, _vp, _vp, _vp, _sz]
     L.bfsim_run_batch.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _vp, _sz]
@@ -77,8 +79,36 @@ def _err():
 
 
 # --------------------------------------------------------------- host batcher
-def sample_instance(seed, *, rate, duration, s_max=64, p=0.02, prefill_kind=0, decode_kind=0, fixed_o=1):
-    """sample_instance (workload.hpp:241-266), byte-identical traces."""
+class _Dist(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("fixed", C.c_int64), ("p", C.c_double),
+                ("values", C.c_void_p), ("n_values", C.c_int64)]
+
+
+def _dist(kind, fixed, p, values):
+    arr = None if values is None else np.ascontiguousarray(values, np.int64)
+    d = _Dist(2 if arr is not None else kind, 0, int(fixed), float(p),
+              arr.ctypes.data if arr is not None else None, 0 if arr is None else arr.shape[0])
+    return d, arr
+
+
+def sample_instance(seed, *, rate, duration, s_max=64, p=0.02, prefill_kind=0, decode_kind=0, fixed_o=1,
+                    prefill_values=None, decode_values=None):
+    """sample_instance (workload.hpp:241-266), byte-identical traces. prefill_values /
+    decode_values select the Empirical distributions (workload.hpp:109-118, 185-193)."""
+    if prefill_values is not None or decode_values is not None:
+        L, err = lib(), _err()
+        pd, pa = _dist(prefill_kind, s_max, 0.0, prefill_values)
+        dd, da = _dist(decode_kind, fixed_o, p, decode_values)
+        n = np.zeros(1, np.int64)
+        rc = L.bfsim_sample_instance_dist(C.byref(pd), C.byref(dd), rate, duration, seed, None, 0, abi.ptr(n), err, 1024)
+        if rc:
+            _raise(rc, err)
+        out = np.zeros(int(n[0]), abi.request_dtype)
+        rc = L.bfsim_sample_instance_dist(C.byref(pd), C.byref(dd), rate, duration, seed, abi.ptr(out), out.shape[0],
+                                          abi.ptr(n), err, 1024)
+        if rc:
+            _raise(rc, err)
+        return out
     L, err = lib(), _err()
     n = np.zeros(1, np.int64)
     rc = L.bfsim_sample_instance(prefill_kind, s_max, decode_kind, p, fixed_o, rate, duration, seed, None, 0, abi.ptr(n), err, 1024)
@@ -91,10 +121,18 @@ def sample_instance(seed, *, rate, duration, s_max=64, p=0.02, prefill_kind=0, d
     return out
 
 
-def sample_stream(seed, n, *, s_max=64, p=0.02, prefill_kind=0, decode_kind=0, fixed_o=1):
+def sample_stream(seed, n, *, s_max=64, p=0.02, prefill_kind=0, decode_kind=0, fixed_o=1, prefill_values=None,
+                  decode_values=None):
     """The (prefill, decode) draws of run_overloaded's top-up (oracle.hpp:177-183)."""
     L, err = lib(), _err()
     out = np.zeros(int(n), abi.sample_dtype)
+    if prefill_values is not None or decode_values is not None:
+        pd, pa = _dist(prefill_kind, s_max, 0.0, prefill_values)
+        dd, da = _dist(decode_kind, fixed_o, p, decode_values)
+        rc = L.bfsim_sample_stream_dist(C.byref(pd), C.byref(dd), seed, int(n), abi.ptr(out), err, 1024)
+        if rc:
+            _raise(rc, err)
+        return out
     rc = L.bfsim_sample_stream(prefill_kind, s_max, decode_kind, p, fixed_o, seed, int(n), abi.ptr(out), err, 1024)
     if rc:
         _raise(rc, err)

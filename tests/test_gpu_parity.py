@@ -340,3 +340,27 @@ def test_pinned_zero_copy_sinks_match(ctx):
         np.testing.assert_array_equal(pb.reqs[key][:n0], ref.requests(0, n0)[key], err_msg=key)
         np.testing.assert_array_equal(pb.reqs[key][-trs[1].shape[0]:], ref.requests(5, trs[1].shape[0])[key],
                                       err_msg=key)
+
+
+def test_empirical_inputs(ctx, orc, ref):
+    """Traces / streams from Empirical prefill and decode lists
+    (workload.hpp:109-118, 185-193) through the engine: Poisson against the
+    oracle, run_overloaded against the unmodified reference drawing the same
+    lists itself (ref_set_empirical)."""
+    pv, dv = [3, 17, 17, 64, 1, 250], [1, 2, 5, 40, 40, 300, 7]
+    tr = host.sample_instance(4, rate=900.0, duration=1.5, prefill_values=pv, decode_values=dv)
+    scs = [abi.scenario(policy=p, workers=8, batch=12, horizon=H) for p, H in
+           ((abi.FCFS, 0), (abi.BFIO_GREEDY, 0), (abi.BFIO_GREEDY, 6))]
+    br = _poisson_batch(ctx, scs, [tr] * 3)
+    for i in range(3):
+        check_poisson(orc, br, i, br.scen[i], tr)
+    ref.set_empirical(pv, dv)
+    stream = host.sample_stream(11, 60000, prefill_values=pv, decode_values=dv)
+    so = abi.scenario(mode=abi.OVERLOADED, policy=abi.BFIO_GREEDY, workers=8, batch=16, horizon=4, steps=80,
+                      warmup=20, seed=11, input_id=0)
+    br = ctx.run_batch(np.array([so], abi.scenario_dtype), host.InputPool([stream]), emit_steps=True)
+    rc, err, (st, rq, m, done) = ref.run_overloaded(br.scen[0], s_max=250, prefill_kind=2, decode_kind=2)
+    assert rc == 0, err
+    np.testing.assert_array_equal(br.steps(0)["loads"], st.loads)
+    for k in EXACT:
+        assert float(br.res[0][k]) == m[k], k
