@@ -361,6 +361,7 @@ def test_empirical_inputs(ctx, orc, ref):
     br = ctx.run_batch(np.array([so], abi.scenario_dtype), host.InputPool([stream]), emit_steps=True)
     rc, err, (st, rq, m, done) = ref.run_overloaded(br.scen[0], s_max=250, prefill_kind=2, decode_kind=2)
     assert rc == 0, err
-    np.testing.assert_array_equal(br.steps(0)["loads"], st.loads)
+    # the reference keeps the records after warm-up (oracle.hpp:229-241); the sink has every step
+    np.testing.assert_array_equal(br.steps(0)["loads"][-st.loads.shape[0]:], st.loads)
     for k in EXACT:
         assert float(br.res[0][k]) == m[k], k
