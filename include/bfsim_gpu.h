@@ -287,6 +287,39 @@ int bfsim_assign_batch(bfsim_ctx_t* ctx, const bfsim_assign_call_t* calls, int64
 int bfsim_iir_reduce(const double* fcfs_trial_means, const double* bfio_trial_means, int32_t trials,
                      int32_t n_cells, double* out, char* err, size_t errlen);
 
+/* ---- device-side input generation ----------------------- */
+/* One synthetic input: sample_instance(prefill, decode, rate, duration, seed)
+ * (workload.hpp:241-266), or -- for the stream calls -- the first `samples`
+ * (prefill, decode) pairs run_overloaded draws from mt19937_64(seed)
+ * (oracle.hpp:177-183; rate/duration ignored). Empirical value lists are host
+ * pointers. Output is byte-identical to bfsim_sample_instance_dist /
+ * bfsim_sample_stream_dist (same libstdc++ draws, glibc's own log). */
+typedef struct bfsim_gen_spec_t {
+  bfsim_dist_t prefill;
+  bfsim_dist_t decode;
+  double rate;
+  double duration;
+  uint64_t seed;
+} bfsim_gen_spec_t;
+/* Pool sizes the generators need: records (traces: a Poisson(rate*duration)
+ * bound per trace, mean + 12 sd + 64; streams: samples each) and class_base
+ * entries (largest possible prefill + 2 each). stream_samples < 0 = traces. */
+int bfsim_generate_bounds(const bfsim_gen_spec_t* specs, int32_t n, int64_t stream_samples, int64_t* n_records,
+                          int64_t* n_class_base, char* err, size_t errlen);
+/* Generate n traces into device memory (one warp per trace), with their
+ * class_base tables; fills inputs_out[n] on the host (what bfsim_prepare_trace
+ * computes), ready for bfsim_run_batch_device. Synchronizes `stream` (the
+ * lengths are needed on the host to plan the run). */
+int bfsim_generate_traces(bfsim_ctx_t* ctx, const bfsim_gen_spec_t* specs, int32_t n, bfsim_request_t* traces_dev,
+                          int64_t n_records, int32_t* class_base_dev, int64_t n_class_base,
+                          bfsim_input_t* inputs_out, void* stream, char* err, size_t errlen);
+int bfsim_generate_streams(bfsim_ctx_t* ctx, const bfsim_gen_spec_t* specs, int32_t n, int64_t samples,
+                           bfsim_sample_t* streams_dev, int64_t n_samples_cap, int32_t* class_base_dev,
+                           int64_t n_class_base, bfsim_input_t* inputs_out, void* stream, char* err,
+                           size_t errlen);
+/* Host twin of the device's glibc log (csrc/libm_log.cuh), for the tests. */
+void bfsim_libm_log_host(const double* x, double* y, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

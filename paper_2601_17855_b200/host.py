@@ -69,6 +69,11 @@ def lib():
     L.bfsim_iir_reduce.argtypes = [_vp, _vp, _i32, _i32, _vp, _vp, _sz]
     L.bfsim_assign_batch.argtypes = [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64,
                                      _vp, _vp, _vp, _vp, _sz]
+    L.bfsim_generate_bounds.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp, _sz]
+    L.bfsim_generate_traces.argtypes = [_vp, _vp, _i32, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _sz]
+    L.bfsim_generate_streams.argtypes = [_vp, _vp, _i32, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _sz]
+    L.bfsim_libm_log_host.argtypes = [_vp, _vp, _i64]
+    L.bfsim_libm_log_host.restype = None
     assert L.bfsim_abi_version() == 1
     _LIB = L
     return L
@@ -178,6 +183,92 @@ class InputPool:
         self.class_base = np.concatenate(cbs).astype(np.int32) if cbs else np.zeros(1, np.int32)
 
 
+class _GenSpec(C.Structure):
+    _fields_ = [("prefill", _Dist), ("decode", _Dist), ("rate", C.c_double), ("duration", C.c_double),
+                ("seed", C.c_uint64)]
+
+
+def libm_log(x):
+    """The host twin of the device's glibc log (csrc/libm_log.cuh)."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    lib().bfsim_libm_log_host(abi.ptr(x), abi.ptr(y), x.size)
+    return y
+
+
+class DevicePool:
+    """Traces (sample_instance, workload.hpp:241-266) or overloaded sample
+    streams (oracle.hpp:177-183) generated in HBM by the device generator
+    (bfsim_generate_traces / bfsim_generate_streams),
+    byte-identical to sample_instance / sample_stream above. Usable wherever an
+    InputPool goes into DeviceBatch; `records` / `class_base` are device
+    tensors, `inputs` the host table the planner needs.
+
+    specs: one dict per input with the keyword arguments of sample_instance
+    (seed, rate, duration, s_max, p, prefill_kind, decode_kind, fixed_o,
+    prefill_values, decode_values); `samples` selects stream mode."""
+
+    def __init__(self, ctx, specs, *, samples=None, stream=None):
+        import torch
+
+        L, err = lib(), _err()
+        self.kind = "stream" if samples is not None else "trace"
+        keep = []
+        arr = (_GenSpec * max(1, len(specs)))()
+        for i, sp in enumerate(specs):
+            pd, pa = _dist(sp.get("prefill_kind", 0), sp.get("s_max", 64), 0.0, sp.get("prefill_values"))
+            dd, da = _dist(sp.get("decode_kind", 0), sp.get("fixed_o", 1), sp.get("p", 0.02), sp.get("decode_values"))
+            keep += [pa, da]
+            arr[i] = _GenSpec(pd, dd, float(sp.get("rate", 1.0)), float(sp.get("duration", 1.0)), int(sp["seed"]))
+        n = len(specs)
+        nrec, ncb = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        rc = L.bfsim_generate_bounds(arr, n, -1 if samples is None else int(samples), abi.ptr(nrec), abi.ptr(ncb),
+                                     err, 1024)
+        if rc:
+            _raise(rc, err)
+        dev = torch.device("cuda", ctx.device)
+        isz = (abi.sample_dtype if samples is not None else abi.request_dtype).itemsize
+        self.records = torch.empty(max(1, int(nrec[0]) * isz), dtype=torch.uint8, device=dev)
+        self.class_base = torch.empty(max(1, int(ncb[0])), dtype=torch.int32, device=dev)
+        self.inputs = np.zeros(n, abi.input_dtype)
+        s = stream if stream is not None else torch.cuda.current_stream(ctx.device)
+        if samples is None:
+            rc = L.bfsim_generate_traces(ctx.h, arr, n, self.records.data_ptr(), int(nrec[0]),
+                                         self.class_base.data_ptr(), int(ncb[0]), abi.ptr(self.inputs),
+                                         C.c_void_p(s.cuda_stream), err, 1024)
+        else:
+            rc = L.bfsim_generate_streams(ctx.h, arr, n, int(samples), self.records.data_ptr(), int(nrec[0]),
+                                          self.class_base.data_ptr(), int(ncb[0]), abi.ptr(self.inputs),
+                                          C.c_void_p(s.cuda_stream), err, 1024)
+        if rc:
+            _raise(rc, err)
+        self.capacity_records = int(nrec[0])
+
+    def host_records(self, i):
+        """Input i copied back to the host (request_dtype / sample_dtype)."""
+        dt = abi.sample_dtype if self.kind == "stream" else abi.request_dtype
+        info = self.inputs[i]
+        a, b = int(info["offset"]) * dt.itemsize, int(info["offset"] + info["length"]) * dt.itemsize
+        return self.records[a:b].cpu().numpy().view(dt)
+
+    def trace_stats(self, i):
+        """(sum of decode lengths, last arrival time, largest decode) of trace i,
+        reduced on the device (the step-sink capacity heuristic)."""
+        import torch
+
+        info = self.inputs[i]
+        a, n = int(info["offset"]), int(info["length"])
+        rec = self.records[a * 16:(a + n) * 16]
+        dec = rec.view(torch.int32).view(n, 4)[:, 3].to(torch.int64)
+        last = float(rec.view(torch.float64).view(n, 2)[-1, 0].item())
+        return int(dec.sum().item()), last, int(info["max_decode"])
+
+    def host_class_base(self, i):
+        info = self.inputs[i]
+        a = int(info["class_base_offset"])
+        return self.class_base[a:a + int(info["s_max"]) + 2].cpu().numpy()
+
+
 # ----------------------------------------------------------------- engine
 class Context:
     """One CUDA device (bfsim_ctx_t). Not thread-safe."""
@@ -284,12 +375,16 @@ def _step_cap(s, pool, explicit):
     N = int(info["length"])
     if N == 0:
         return 1
-    recs = pool.records[int(info["offset"]): int(info["offset"]) + N]
-    work = int(np.asarray(recs["decode"], np.int64).sum())
+    if isinstance(pool, DevicePool):
+        work, last, omax = pool.trace_stats(int(s["input_id"]))
+    else:
+        recs = pool.records[int(info["offset"]): int(info["offset"]) + N]
+        work = int(np.asarray(recs["decode"], np.int64).sum())
+        last, omax = float(recs["arrival_time"][-1]), int(recs["decode"].max())
     G, B = int(s["workers"]), int(s["batch"])
-    span = float(recs["arrival_time"][-1]) / max(float(s["overhead"]), 1e-6)
+    span = last / max(float(s["overhead"]), 1e-6)
     # heuristic capacity; run_batch re-runs any scenario that overflows it
-    bound = int(span) + (3 * work) // (2 * max(1, G * B)) + int(recs["decode"].max()) + 64
+    bound = int(span) + (3 * work) // (2 * max(1, G * B)) + omax + 64
     return int(min(int(s["max_steps"]), bound))
 
 
@@ -351,8 +446,11 @@ class DeviceBatch:
             return t
 
         self._keep = []
-        self.records = dbuf(pool.records)
-        self.class_base = dbuf(pool.class_base)
+        if isinstance(pool, DevicePool):  # already resident in HBM
+            self.records, self.class_base = pool.records, pool.class_base
+        else:
+            self.records = dbuf(pool.records)
+            self.class_base = dbuf(pool.class_base)
         self.is_stream = pool.kind == "stream"
         self.pool = pool
         self.steps = self.reqs = None
