@@ -10,6 +10,10 @@ from hotlines import main as _unused  # noqa: F401  (same CSV format)
 
 SRC = __file__.rsplit("/", 2)[0] + "/paper_2601_17855_b200/csrc/engine_impl.cuh"
 MARKS = [
+    (r"^__device__ __forceinline__ uint64_t mt_temper", "noisy: producer warp (mt19937_64, polar)"),
+    (r"^template <bool SM, class T>", "setup / other"),
+    (r"^struct WideChain", "wide chain (G > 128)"),
+    (r"^template <int MODE, int POL, int WPL, bool SMALLC, bool SM, bool NOISY, int HR, bool WIDE = false>", "setup / other"),
     (r"auto drain_tpot = ", "accounting (flush, TPOT)"),
     (r"auto reveal = ", "reveal"),
     (r"auto topup = ", "overloaded top-up"),

@@ -8,7 +8,7 @@ OUT=gpurun_out/sanitizer.txt
 run() {  # tool, label, command...
   local tool=$1 label=$2; shift 2
   echo "== $tool: $label" >> $OUT
-  timeout 600 compute-sanitizer --tool $tool --print-limit 10 "$@" 2>&1 | grep -E "ERROR SUMMARY|RACECHECK SUMMARY|Error|error|ok|smoke" | tail -4 >> $OUT
+  timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 10 "$@" 2>&1 | grep -E "SUMMARY|Error|error|ok|smoke|No such|not found" | tail -4 >> $OUT
 }
 for tool in memcheck racecheck synccheck; do
   run $tool "smoke (fcfs, jsq, greedy H=0/4, noisy H=8, calendar, overloaded)" python -c "import __graft_entry__ as g; g.smoke()"
