@@ -62,6 +62,8 @@ struct bfsim_ctx {
   DevBuf order, ws, queue;
   // batched assign()
   DevBuf a_calls, a_pv, a_fut, a_caps, a_cnt, a_pairs, a_np, a_cost, a_st, a_ws;
+  // dyadic-drift inputs: prefill-scaled copies of traces / streams / class_base
+  DevBuf dy_tr, dy_sm, dy_cb;
   int64_t last_launches = 0;
   bool timed = false;
 
@@ -75,6 +77,48 @@ int cuda_fail(char* err, size_t errlen, cudaError_t e, const char* what) {
 }
 
 bool is_int_drift(double v) { return v >= 0.0 && v == std::floor(v) && v < 1e9; }
+
+// Dyadic constant drift d = m / 2^e (SURVEY hard part 2). The reference
+// accumulates the profile sequentially in fp64 (drift_profile,
+// workload.hpp:73-85); with a dyadic d every partial sum s + j*d is exact, so
+// the run equals the integer problem with every workload scaled by 2^e
+// (prefill s*2^e, drift m): loads, maxima and the policies' sums scale
+// exactly, every comparison and tie is unchanged, t_ell*2^-e times the scaled
+// maximum is the reference's dt bit for bit, and the kernel scales the loads
+// back on the way out (engine_impl.cuh, lsc).
+constexpr int kMaxDriftShift = 16;
+constexpr int kMaxScaledClasses = 262143;  // ClassSet<false>: 3-level 64-ary bitmap
+bool dyadic_drift(double v, int64_t* m, int* e) {
+  if (!(v >= 0.0) || !std::isfinite(v)) return false;
+  for (int k = 0; k <= kMaxDriftShift; ++k) {
+    const double x = std::ldexp(v, k);
+    if (x == std::floor(x)) {
+      if (x >= 1e9) return false;
+      *m = static_cast<int64_t>(x);
+      *e = k;
+      return true;
+    }
+  }
+  return false;
+}
+
+template <class R>
+__global__ void scale_prefill_kernel(const R* __restrict__ src, R* __restrict__ dst, int64_t n, int e) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    R r = src[i];
+    r.prefill <<= e;
+    dst[i] = r;
+  }
+}
+
+// class_base of the scaled input: #records with s*2^e < c = #records with s < ceil(c / 2^e)
+__global__ void scale_class_base_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n,
+                                        int e) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < n;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[c] = src[(c + (int64_t{1} << e) - 1) >> e];
+}
 
 // SimConfig::validate (engine.hpp:31-36), PowerModel::validate
 // (metrics_power.hpp:17-21), DriftSpec::validate (workload.hpp:52-60), plus the
@@ -94,9 +138,12 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
   if (!(s.gamma > 0.0 && s.gamma < 1.0))
     return fail(err, errlen, BFSIM_EINVAL, "power: gamma out of (0,1)");
   if (s.drift < 0.0) return fail(err, errlen, BFSIM_EINVAL, "drift: increment out of [0, delta_max]");
-  if (!is_int_drift(s.drift))
+  int64_t d = 0;
+  int dshift = 0;
+  if (!dyadic_drift(s.drift, &d, &dshift))
     return fail(err, errlen, BFSIM_EINVAL,
-                "drift: the GPU path is bit-exact only for integer constant drift (SURVEY F5)");
+                "drift: the GPU path is bit-exact only for integer or dyadic (m / 2^e, e <= 16) constant drift "
+                "(SURVEY F5)");
   if (s.policy == BFSIM_POLICY_BFIO_EXACT)
     return fail(err, errlen, BFSIM_EINVAL,
                 "bfio-exact is an exponential search; it runs on the CPU reference only");
@@ -128,8 +175,9 @@ int validate_scenario(const bfsim_scenario_t& s, const bfsim_input_t* inputs, in
       return fail(err, errlen, BFSIM_EINVAL, "run_overloaded: too many steps");
   }
   if (s.horizon > 4096) return fail(err, errlen, BFSIM_EINVAL, "GPU path: horizon > 4096");
-  const bfsim_input_t& in = inputs[s.input_id];
-  const int64_t d = static_cast<int64_t>(s.drift);
+  // bounds on the (dyadic-scaled) integer problem
+  bfsim_input_t in = inputs[s.input_id];
+  in.s_max = static_cast<int32_t>(std::min<int64_t>(static_cast<int64_t>(in.s_max) << dshift, INT32_MAX));
   const double lb = static_cast<double>(s.batch) *
                     (static_cast<double>(in.s_max) + static_cast<double>(d) * (in.max_decode - 1));
   if (lb >= 2147483647.0)
@@ -187,6 +235,10 @@ int chain_kind(const bfsim_scenario_t& s, const bfsim_input_t& in, int noisy) {
   if (s.policy == BFSIM_POLICY_BFIO_GREEDY && s.horizon > 0 && !noisy && s.workers > 128) return 1;
   return 0;
 }
+
+// int32 chain views (engine_impl.cuh, HP): G worker rows of H + 1 int32
+// words rounded up to 4 (128-bit row loads)
+int64_t chain_rows_bytes(int H, int G) { return static_cast<int64_t>(G) * ((H + 4) & ~3) * 4; }
 
 int wpl_for(int G) {
   int w = (G + 31) / 32;
@@ -282,10 +334,13 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
     items.push_back({&p.o_pre, (G + 1) * 4LL, true});
     items.push_back({&p.o_Wc, static_cast<int64_t>(H) * G * 4, true});
     items.push_back({&p.o_Wa, static_cast<int64_t>(H) * G * 4, true});
-    if (g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
+    if (g.hr) items.push_back({&p.o_F, chain_rows_bytes(H, G), true});
   }
   // int32 views (register-budget and wide chains)
-  if (greedy && H > 0 && !g.noisy && g.hr) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});
+  if (greedy && H > 0 && !g.noisy && g.hr) {
+    if (g.hr == 1) items.push_back({&p.o_F, (H + 1) * 4LL * G, true});  // wide chain: [h][g]
+    else items.push_back({&p.o_F, chain_rows_bytes(H, G), true});
+  }
   if (greedy && H > 0 && g.hr) items.push_back({&p.o_admc, G * 4LL, true});
   // per-slot state touched every step (retire)
   items.push_back({&p.o_f, ((GB + 3) & ~3LL) * 4});
@@ -415,7 +470,8 @@ void bfsim_ctx_destroy(bfsim_ctx_t* c) {
                     &c->st_cs,   &c->st_dt,  &c->st_mx,  &c->st_ac,  &c->st_ld,   &c->rq_as,
                     &c->rq_ss,   &c->rq_wk,  &c->rq_ac,  &c->rq_fc,  &c->order,   &c->ws,
                     &c->queue,   &c->a_calls, &c->a_pv,  &c->a_fut,  &c->a_caps,  &c->a_cnt,
-                    &c->a_pairs, &c->a_np,   &c->a_cost, &c->a_st,   &c->a_ws};
+                    &c->a_pairs, &c->a_np,   &c->a_cost, &c->a_st,   &c->a_ws,
+                    &c->dy_tr,   &c->dy_sm,  &c->dy_cb};
   for (auto* b : bufs) b->release();
   for (int i = 0; i < kMaxGroups; ++i) {
     cudaStreamDestroy(c->side[i]);
@@ -458,6 +514,44 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
   cudaSetDevice(ctx->device);
   // scenarios must refer to device-resident scenario rows for the kernel: copy
   cudaStream_t us = static_cast<cudaStream_t>(stream);
+  // dyadic drift: such scenarios run on prefill-scaled copies of their inputs
+  // (dyadic_drift above); the kernel reads the shift from reserved0
+  std::vector<bfsim_scenario_t> scen2(scen_host, scen_host + n_scen);
+  std::vector<bfsim_input_t> inputs2(inputs_host, inputs_host + n_inputs);
+  struct DyJob {
+    int32_t src, dst;
+    int e, mode;
+  };
+  std::vector<DyJob> dy;
+  {
+    std::map<std::tuple<int32_t, int, int>, int32_t> ids;
+    for (auto& s : scen2) {
+      s.reserved0 = 0;
+      int64_t m = 0;
+      int e = 0;
+      if (is_int_drift(s.drift) || !dyadic_drift(s.drift, &m, &e) || s.input_id < 0 || s.input_id >= n_inputs)
+        continue;  // integer drift, or validate_scenario reports it
+      const auto key = std::make_tuple(s.input_id, e, s.mode);
+      auto it = ids.find(key);
+      if (it == ids.end()) {
+        bfsim_input_t in = inputs_host[s.input_id];
+        if ((static_cast<int64_t>(in.s_max) << e) > kMaxScaledClasses)
+          return fail(err, errlen, BFSIM_EINVAL, "drift: dyadic drift needs s_max * 2^e <= 262143 on the GPU path");
+        in.s_max <<= e;
+        const int32_t id = static_cast<int32_t>(inputs2.size());
+        inputs2.push_back(in);
+        dy.push_back({s.input_id, id, e, s.mode});
+        it = ids.emplace(key, id).first;
+      }
+      s.drift = static_cast<double>(m);
+      s.per_token = std::ldexp(s.per_token, -e);
+      s.reserved0 = e;
+      s.input_id = it->second;
+    }
+  }
+  scen_host = scen2.data();
+  inputs_host = inputs2.data();
+  n_inputs = static_cast<int32_t>(inputs2.size());
   for (int64_t i = 0; i < n_scen; ++i) {
     int rc = validate_scenario(scen_host[i], inputs_host, n_inputs, nullptr, err, errlen);
     if (rc) {
@@ -469,6 +563,59 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
       return fail(err, errlen, BFSIM_EINVAL, "poisson scenario without traces");
     if (scen_host[i].mode == BFSIM_MODE_OVERLOADED && !streams_dev)
       return fail(err, errlen, BFSIM_EINVAL, "overloaded scenario without sample streams");
+  }
+  int64_t dy_launches = 0;
+  if (!dy.empty()) {
+    int64_t n_tr = 0, n_sm = 0, n_cb = 0;
+    for (const auto& j : dy) {
+      (j.mode == BFSIM_MODE_POISSON ? n_tr : n_sm) += inputs2[j.src].length;
+      n_cb += inputs2[j.dst].s_max + 2;
+    }
+    cudaError_t e;
+    if ((e = ctx->dy_tr.ensure(std::max<int64_t>(n_tr, 1) * sizeof(bfsim_request_t))) != cudaSuccess ||
+        (e = ctx->dy_sm.ensure(std::max<int64_t>(n_sm, 1) * sizeof(bfsim_sample_t))) != cudaSuccess ||
+        (e = ctx->dy_cb.ensure(n_cb * 4)) != cudaSuccess)
+      return cuda_fail(err, errlen, e, "dyadic-drift input alloc");
+    // the scaled copies are addressed from the caller's pool bases (offsets
+    // across allocations in the flat device address space)
+    auto rel = [](const void* p, const void* base, size_t rec, int64_t* off) {
+      const intptr_t d = reinterpret_cast<intptr_t>(p) - reinterpret_cast<intptr_t>(base);
+      if (d % static_cast<intptr_t>(rec)) return false;
+      *off = static_cast<int64_t>(d / static_cast<intptr_t>(rec));
+      return true;
+    };
+    int64_t o_tr = 0, o_sm = 0, o_cb = 0;
+    for (const auto& j : dy) {
+      const bfsim_input_t& src = inputs2[j.src];
+      bfsim_input_t& dst = inputs2[j.dst];
+      const int blocks = static_cast<int>(std::min<int64_t>(4 * ctx->sm_count, (src.length + 255) / 256 + 1));
+      bool ok;
+      if (j.mode == BFSIM_MODE_POISSON) {
+        auto* out = static_cast<bfsim_request_t*>(ctx->dy_tr.p) + o_tr;
+        ok = rel(out, traces_dev, sizeof(bfsim_request_t), &dst.offset);
+        if (ok && src.length > 0) {
+          scale_prefill_kernel<<<blocks, 256, 0, us>>>(traces_dev + src.offset, out, src.length, j.e);
+          ++dy_launches;
+        }
+        o_tr += src.length;
+      } else {
+        auto* out = static_cast<bfsim_sample_t*>(ctx->dy_sm.p) + o_sm;
+        ok = rel(out, streams_dev, sizeof(bfsim_sample_t), &dst.offset);
+        if (ok && src.length > 0) {
+          scale_prefill_kernel<<<blocks, 256, 0, us>>>(streams_dev + src.offset, out, src.length, j.e);
+          ++dy_launches;
+        }
+        o_sm += src.length;
+      }
+      int32_t* cb = static_cast<int32_t*>(ctx->dy_cb.p) + o_cb;
+      ok = ok && rel(cb, class_base_dev, 4, &dst.class_base_offset);
+      if (!ok) return fail(err, errlen, BFSIM_ECUDA, "dyadic drift: misaligned input pool");
+      scale_class_base_kernel<<<static_cast<int>((dst.s_max + 2 + 255) / 256), 256, 0, us>>>(
+          class_base_dev + src.class_base_offset, cb, dst.s_max + 2, j.e);
+      ++dy_launches;
+      o_cb += dst.s_max + 2;
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(err, errlen, e, "dyadic-drift input scaling");
   }
   // group by kernel variant; LPT order inside a group
   std::map<std::tuple<int, int, int, int, int, int>, Group> groups;
@@ -551,7 +698,7 @@ int run_batch_device_impl(bfsim_ctx_t* ctx, const bfsim_scenario_t* scen_host, i
   cudaMemcpyAsync(ctx->inputs.p, inputs_host, n_inputs * sizeof(bfsim_input_t), cudaMemcpyHostToDevice, us);
   cudaMemcpyAsync(ctx->order.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice, us);
   cudaMemsetAsync(ctx->queue.p, 0, std::max<size_t>(gl.size(), 1) * 4, us);
-  int64_t launches = 0;  // counted below: kernels only (not copies / memsets)
+  int64_t launches = dy_launches;  // kernels only (not copies / memsets)
   cudaEventRecord(ctx->t0, us);
   cudaEventRecord(ctx->fork, us);
   int64_t off = 0, ws_off = 0;

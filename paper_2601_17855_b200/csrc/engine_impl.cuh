@@ -169,6 +169,24 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.cta.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// L2 residency hints for the noisy per-worker lists (read and rewritten every
+// step, ~32 KB per trajectory in the global workspace): evict_last keeps them
+// in L2 ahead of the streaming data (deques, traces, draw scratch)
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int2 ld_keep(const int2* ptr, uint64_t pol) {
+  int2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(int2* ptr, int2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.s32 [%0], {%1, %2}, %3;" ::"l"(ptr), "r"(v.x), "r"(v.y), "l"(pol)
+               : "memory");
+}
+
 // Noisy lookahead draw stream (make_preview, policies.hpp:74-76). Every step
 // the reference draws normal_distribution(0, sigma) values from the
 // simulation's mt19937_64 -- one per active request, then one per waiting
@@ -570,6 +588,9 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   const bfsim_sample_t* st = P.streams ? P.streams + in.offset : nullptr;
   const int32_t* cbase_g = P.class_base + in.class_base_offset;
   const double C0 = sc.overhead, TL = sc.per_token;
+  // dyadic drift m / 2^e: the host scaled every workload by 2^e (and t_ell by
+  // 2^-e, capi.cu scale_dyadic); loads leave the kernel scaled back, exactly
+  const double lsc = sc.reserved0 > 0 ? ldexp(1.0, -sc.reserved0) : 1.0;
   const double p_idle = sc.p_idle, p_diff = sc.p_max - sc.p_idle, gam = sc.gamma;
   const long long warmup = OVL ? sc.warmup : 0;
   const long long total_steps =
@@ -613,6 +634,12 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int32_t* lvK = at<SM || !GREEDY, int32_t>(sm, ws, pl.o_lvK);
   uint32_t* lvM = at<SM || !GREEDY, uint32_t>(sm, ws, pl.o_lvM);
   long long* s_F = at<SM || (HR > 0) || WIDE, long long>(sm, ws, pl.o_F);
+  // int32 chain (HR > 0): views F_h[g] worker-major, row g = F_0..F_{HP-1}
+  // (zero past H), HP = the group's H + 1 rounded up to 4 words, so a lane
+  // reads 4 horizons of its worker per 128-bit load (capi.cu
+  // chain_rows_bytes). The wide chain keeps [h][g].
+  const int HP = (pl.H + 4) & ~3;
+  constexpr int HP4MAX = HR > 8 ? 6 : 2;  // H < HR
   long long* s_M = at<SM || GREEDY, long long>(sm, ws, pl.o_M);
   int32_t* s_Wc = at<SM || NOISY, int32_t>(sm, ws, pl.o_Wc);
   long long* s_Wa = at<SM || NOISY, long long>(sm, ws, pl.o_Wa);
@@ -644,6 +671,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int* s_ring = NOISY ? at<true, int>(sm, ws, pl.o_nring) : nullptr;  // the producer warp's draws
   unsigned* s_ctr = NOISY ? at<true, unsigned>(sm, ws, pl.o_misc) + 1 : nullptr;
   int2* s_E = NOISY ? gat<int2>(ws, pl.o_lst) : nullptr;
+  const uint64_t lkeep = NOISY ? l2_keep_policy() : 0;
   int32_t* s_Eid = NOISY ? gat<int32_t>(ws, pl.o_eid) : nullptr;
   int32_t* s_pre = NOISY ? at<true, int32_t>(sm, ws, pl.o_pre) : nullptr;
   int32_t* n_Wa = NOISY ? reinterpret_cast<int32_t*>(s_Wa) : nullptr;
@@ -805,7 +833,7 @@ BFSIM_UNROLL_W
       if (emit_steps && kk < scap) {
         P.steps.clock_start[so + kk] = r_cs[lane];
         P.steps.dt[so + kk] = dt;
-        P.steps.max_load[so + kk] = mxd;
+        P.steps.max_load[so + kk] = mxd * lsc;
         P.steps.active_count[so + kk] = r_ac[lane];
       }
     }
@@ -827,7 +855,7 @@ BFSIM_UNROLL_W
       long long rows = scap - k0 < cnt ? scap - k0 : cnt;
       for (long long r = 0; r < rows; ++r)
         for (int g = lane; g < G; g += 32)
-          P.steps.loads[lo + (k0 + r) * G + g] = static_cast<double>(r_l[r * rstride + g]);
+          P.steps.loads[lo + (k0 + r) * G + g] = static_cast<double>(r_l[r * rstride + g]) * lsc;
     }
     __syncwarp();
   };
@@ -982,7 +1010,7 @@ BFSIM_UNROLL_W
     s_a[slot] = static_cast<int32_t>(s - d * k);
     if constexpr (NOISY) {  // appended after the worker's active entries (sorted by id below)
       const int pos = g * B + (B - s_capb[g]) + rank;
-      s_E[pos] = make_int2(static_cast<int>(k + o - 1), static_cast<int>(s - d * k));
+      st_keep(s_E + pos, make_int2(static_cast<int>(k + o - 1), static_cast<int>(s - d * k)), lkeep);
       s_Eid[pos] = static_cast<int32_t>(id);
     }
     s_x[slot] = static_cast<int32_t>(k);
@@ -1030,7 +1058,7 @@ BFSIM_UNROLL_W
         while (nx <= r) nx = s_pre[++g + 1];
         gq = g;
         gn = g;
-        en = s_E[g * B + static_cast<int>(r - s_pre[g])];
+        en = ld_keep(s_E + g * B + static_cast<int>(r - s_pre[g]), lkeep);
       };
       if (lane < act) fetch(lane);
       for (long long r0 = 0; r0 < D; r0 += 32) {
@@ -1601,8 +1629,11 @@ BFSIM_UNROLL_W
             }
             const long long kh = k + h;
             const long long F = trunc ? A[j] + d * kh * n[j] - d * Q : (A[j] + d * kh * n[j]) - (PA + d * kh * PC);
-            s_F32[h * G + g] = static_cast<int32_t>(F);
+            if constexpr (HR > 0) s_F32[g * HP + h] = static_cast<int32_t>(F);
+            else s_F32[h * G + g] = static_cast<int32_t>(F);
           }
+          if constexpr (HR > 0)
+            for (int h = H + 1; h < HP; ++h) s_F32[g * HP + h] = 0;
         }
       }
       if constexpr (!NOISY && HR == 0 && !WIDE) {
@@ -1696,13 +1727,22 @@ BFSIM_UNROLL_W
             if (g >= G) continue;
             long long SW = A[j] + d * k * n[j];
             long long CN = n[j];
-            s_F32[g] = static_cast<int32_t>(SW);
-            for (int h = 1; h <= H; ++h) {
-              SW += n_Wa[(h - 1) * G + g];
-              CN += s_Wc[(h - 1) * G + g];
-              n_Wa[(h - 1) * G + g] = 0;
-              s_Wc[(h - 1) * G + g] = 0;
-              s_F32[h * G + g] = static_cast<int32_t>(SW + d * h * CN);
+            int4* row = reinterpret_cast<int4*>(s_F32 + g * HP);
+            int32_t v[4];
+            v[0] = static_cast<int32_t>(SW);
+#pragma unroll
+            for (int h = 1; h < 4 * HP4MAX; ++h) {
+              if (h >= HP) break;
+              if (h <= H) {
+                SW += n_Wa[(h - 1) * G + g];
+                CN += s_Wc[(h - 1) * G + g];
+                n_Wa[(h - 1) * G + g] = 0;
+                s_Wc[(h - 1) * G + g] = 0;
+                v[h & 3] = static_cast<int32_t>(SW + d * h * CN);
+              } else {
+                v[h & 3] = 0;
+              }
+              if ((h & 3) == 3) row[h >> 2] = make_int4(v[0], v[1], v[2], v[3]);
             }
           }
         }
@@ -1711,7 +1751,7 @@ BFSIM_UNROLL_W
         int32_t Ml = 0;              // M_lane
         if (hl)
           for (int g = 0; g < G; ++g) {
-            const int32_t v = s_F32[lane * G + g];
+            const int32_t v = s_F32[g * HP + lane];
             Ml = v > Ml ? v : Ml;
           }
         // The chain's per-worker state is in shared memory too (lane-owned
@@ -1743,26 +1783,34 @@ BFSIM_UNROLL_W
 BFSIM_UNROLL_W
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
-            F0v[j] = g < G ? s_F32[g] : 0;
+            F0v[j] = g < G ? s_F32[g * HP] : 0;
             fre[j] = g < G && s_cap[g] > 0;
             const key_t kk = (static_cast<key_t>(static_cast<uint32_t>(F0v[j])) << gbits) | static_cast<key_t>(g);
             if (fre[j] && kk < fk) fk = kk;
           }
           int gs = static_cast<int>(wmin(fk) & static_cast<key_t>(gmask));
-          int32_t Fg = hl ? s_F32[lane * G + gs] : 0;
+          int32_t Fg = hl ? s_F32[gs * HP + lane] : 0;
           if (__any_sync(FULLMASK, hl && Fg + wl > Ml)) {
-            const int32_t Tl = Ml - wl;
+            // T_h = M_h - w_h (zero past H, like the rows) to the T row,
+            // then every lane scans its workers' rows 4 horizons per load
+            int32_t* s_T = reinterpret_cast<int32_t*>(s_M);  // the shared chain's M/T/w rows are unused here
+            if (lane < HP) s_T[lane] = hl ? Ml - wl : 0;
+            __syncwarp();
             uint32_t cost[WPL];
-            const int32_t* col = s_F32 + (lane < G ? lane : 0);  // this lane's column, row h at h * G
 BFSIM_UNROLL_W
             for (int j = 0; j < WPL; ++j) cost[j] = 0;
-#pragma unroll 4
-            for (int h = 0; h <= H; ++h, col += G) {
-              const int32_t T = __shfl_sync(FULLMASK, Tl, h);
+            const int nh4 = (H + 4) >> 2;
+#pragma unroll
+            for (int h4 = 0; h4 < HP4MAX; ++h4) {
+              if (h4 < nh4) {
+                const int4 T = reinterpret_cast<const int4*>(s_T)[h4];
 BFSIM_UNROLL_W
-              for (int j = 0; j < WPL; ++j) {
-                const int32_t f = lane + 32 * j < G ? col[32 * j] : 0;
-                cost[j] += static_cast<uint32_t>(T > f ? T : f);
+                for (int j = 0; j < WPL; ++j) {
+                  const int g = lane + 32 * j;
+                  const int4 f = reinterpret_cast<const int4*>(s_F32 + (g < G ? g : 0) * HP)[h4];
+                  cost[j] += static_cast<uint32_t>(T.x > f.x ? T.x : f.x) + static_cast<uint32_t>(T.y > f.y ? T.y : f.y) +
+                             static_cast<uint32_t>(T.z > f.z ? T.z : f.z) + static_cast<uint32_t>(T.w > f.w ? T.w : f.w);
+                }
               }
             }
             uint64_t best = ~0ull;
@@ -1775,13 +1823,13 @@ BFSIM_UNROLL_W
               if (fre[j] && key < best) best = key;
             }
             gs = static_cast<int>(wmin_u64(best) & gmask);
-            Fg = hl ? s_F32[lane * G + gs] : 0;
+            Fg = hl ? s_F32[gs * HP + lane] : 0;
           }
           // lane h adds w_h to the chosen row (row 0: its F_0) and raises
           // M_h; the owner lane books the admission
           if (hl) {
             const int32_t v = Fg + wl;
-            s_F32[lane * G + gs] = v;
+            s_F32[gs * HP + lane] = v;
             Ml = v > Ml ? v : Ml;
           }
           if (lane == (gs & 31)) {
@@ -2131,17 +2179,17 @@ BFSIM_UNROLL_W
             int w = 0;
             for (int p0 = 0; p0 < nold; p0 += 64) {  // two chunks in flight
               const int p = p0 + lane, p2 = p0 + 32 + lane;
-              const int2 e = p < nold ? Eg[p] : make_int2(0, 0);
-              const int2 e2 = p2 < nold ? Eg[p2] : make_int2(0, 0);
+              const int2 e = p < nold ? ld_keep(Eg + p, lkeep) : make_int2(0, 0);
+              const int2 e2 = p2 < nold ? ld_keep(Eg + p2, lkeep) : make_int2(0, 0);
               const bool keep = p < nold && static_cast<uint32_t>(e.x) != kf;
               const bool keep2 = p2 < nold && static_cast<uint32_t>(e2.x) != kf;
               const unsigned km = __ballot_sync(FULLMASK, keep);
               const unsigned km2 = __ballot_sync(FULLMASK, keep2);
               // in place: an entry moves only to a lower position, and the
               // second chunk's reads are done before any store
-              if (keep) Eg[w + __popc(km & lanemask_lt())] = e;
+              if (keep) st_keep(Eg + w + __popc(km & lanemask_lt()), e, lkeep);
               w += __popc(km);
-              if (keep2) Eg[w + __popc(km2 & lanemask_lt())] = e2;
+              if (keep2) st_keep(Eg + w + __popc(km2 & lanemask_lt()), e2, lkeep);
               w += __popc(km2);
             }
           }
@@ -2302,12 +2350,12 @@ BFSIM_UNROLL_W
       r.imb_total = r.total_workload = r.eta_sum = 0.0;
     } else {
       // compute_metrics, metrics.hpp:106-122
-      r.avg_imbalance = static_cast<double>(imb) / static_cast<double>(records);
+      r.avg_imbalance = static_cast<double>(imb) * lsc / static_cast<double>(records);
       r.throughput = static_cast<double>(tok) / elapsed;
       r.tpot = done > 0 ? tpot_sum / static_cast<double>(done) : 0.0;
       r.energy = energy;
-      r.imb_total = static_cast<double>(imb);
-      r.total_workload = static_cast<double>(work);
+      r.imb_total = static_cast<double>(imb) * lsc;
+      r.total_workload = static_cast<double>(work) * lsc;
       r.eta_sum = work > 0 ? static_cast<double>(imb) / static_cast<double>(work) : 0.0;
     }
     P.results[si] = r;

@@ -89,3 +89,47 @@ def test_exact_unit_cases(ctx, ref):
     out = host.assign_batch(ctx, lim, search_limit=100)
     assert out[0][2] == abi.ELIMIT
     _check(ctx, ref, lim, limit=100)
+
+
+def _c02_instances(rng, n):
+    """Acceptance C02's instance family (acceptance_test.cpp:130-155): (G, B)
+    in {(2,1), (3,1), (4,1), (2,2)}, s_max in 3..5, a pool over empty workers
+    grown until Def. 1 holds for every slot (is_overloaded_at,
+    workload.hpp:325-336; restarted past 9 requests), H = 0, w_0 = s."""
+    combos = ((2, 1), (3, 1), (4, 1), (2, 2))
+    out = []
+    for _ in range(n):
+        G, B = combos[int(rng.integers(0, 4))]
+        s_max = 3 + int(rng.integers(0, 3))
+        slots = G * B
+        pool = []
+        while True:
+            cnt = np.bincount(np.array(pool, np.int64), minlength=s_max + 1) if pool else np.zeros(s_max + 1)
+            if len(pool) - int(cnt[1:].max()) >= slots:
+                break
+            if len(pool) >= 9:
+                pool = []
+            pool.append(int(rng.integers(1, s_max + 1)))
+        pv = np.array(pool, np.float64).reshape(-1, 1)
+        out.append((s_max, (abi.BFIO_EXACT, pv, np.full(G, B, np.int32), np.zeros(G, np.int32),
+                             np.zeros((G, 1)))))
+    return out
+
+
+def test_c02_smax_balance(ctx, ref):
+    """Acceptance C02 (acceptance_test.cpp:130-169) on the GPU policy operator:
+    1,000 overloaded pools over empty workers, bfio-exact fills every slot and
+    leaves a post-admission load gap <= s_max; each optimum equals the
+    reference's assign() call."""
+    inst = _c02_instances(np.random.default_rng(202), 1000)
+    calls = [c for _, c in inst]
+    got = host.assign_batch(ctx, calls, search_limit=500000)
+    for (s_max, (pol, pv, caps, cnt, fut)), (pairs, cost, st) in zip(inst, got):
+        assert st == abi.OK
+        G = caps.shape[0]
+        assert len(pairs) == int(caps.sum())
+        loads = np.zeros(G)
+        for i, g in pairs:
+            loads[g] += pv[i, 0]
+        assert loads.max() - loads.min() <= s_max
+    _check(ctx, ref, calls[:300], limit=500000)
