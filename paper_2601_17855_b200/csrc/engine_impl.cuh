@@ -1061,6 +1061,13 @@ BFSIM_UNROLL_W
         en = ld_keep(s_E + g * B + static_cast<int>(r - s_pre[g]), lkeep);
       };
       if (lane < act) fetch(lane);
+      // loop-local copies (the kernel-wide ones live in spilled registers) and
+      // 32-bit arithmetic: every quantity below is a step count, a clamped
+      // draw or a per-request workload, all < 2^31 (capi.cu bounds)
+      const unsigned cn = cons;
+      const int32_t kk32 = static_cast<int32_t>(k), d32 = static_cast<int32_t>(d), H1 = H + 1;
+      const int32_t dk32 = static_cast<int32_t>(d * k);
+      unsigned tie = 0;
       for (long long r0 = 0; r0 < D; r0 += 32) {
         const long long r = r0 + lane;
         const int gc = gn;
@@ -1074,33 +1081,35 @@ BFSIM_UNROLL_W
         if (__any_sync(FULLMASK, need)) {
           // everything before r0 is consumed: release it first (the producer
           // may be waiting for room), then wait for this chunk's draws
-          if (lane == 0) st_release(&s_ctr[1], cons + static_cast<unsigned>(r0));
-          const unsigned hi = cons + static_cast<unsigned>(r0 + 32 < D ? r0 + 32 : D);
+          if (lane == 0) st_release(&s_ctr[1], cn + static_cast<unsigned>(r0));
+          const unsigned hi = cn + static_cast<unsigned>(r0 + 32 < D ? r0 + 32 : D);
           for (int spin = 0; static_cast<int>(ld_acquire(&s_ctr[0]) - hi) < 0; ++spin) {
             if (spin > (1 << 26)) __trap();  // the producer never stalls this long: fail, do not hang
             __nanosleep(32);
           }
           if (need) {
-            const int code = s_ring[(cons + static_cast<unsigned>(r)) & (kRing - 1)];
-            const long long lr = code >> 1;
-            if (code & 1) ntie = true;
+            const int code = s_ring[(cn + static_cast<unsigned>(r)) & (kRing - 1)];
+            const int32_t lr = code >> 1;
+            tie |= static_cast<unsigned>(code) & 1u;
             if (r >= act) {
-              nzb[r] = static_cast<int32_t>(lr);
+              nzb[r] = lr;
             } else {
               const int g = gc;
-              const long long f = static_cast<uint32_t>(ec.x);
-              const long long a = ec.y;
-              const long long rem = f - k + 1;
-              long long pred = rem + lr;
+              const int32_t f = ec.x;
+              const int32_t a = ec.y;
+              const int32_t rem = f - kk32 + 1;
+              int32_t pred = rem + lr;
               pred = pred > 1 ? pred : 1;
-              const long long c = pred < H + 1 ? pred : H + 1;
-              const long long m = c < rem ? c : rem;
+              const int32_t c = pred < H1 ? pred : H1;
+              const int32_t m = c < rem ? c : rem;
               if (m <= H) {
-                atomicAdd(&n_Wa[(m - 1) * G + g], static_cast<int32_t>(-(a + d * k)));
+                atomicAdd(&n_Wa[(m - 1) * G + g], -(a + dk32));
                 atomicAdd(&s_Wc[(m - 1) * G + g], -1);
               }
               if (c > rem) {
-                const int32_t wl = static_cast<int32_t>(a + d * f);
+                // the last workload a + d*f < 2^31; the product alone may not be
+                const int32_t wl = static_cast<int32_t>(static_cast<uint32_t>(a) +
+                                                        static_cast<uint32_t>(d32) * static_cast<uint32_t>(f));
                 atomicAdd(&n_Wa[(rem - 1) * G + g], wl);
                 if (c <= H) atomicAdd(&n_Wa[(c - 1) * G + g], -wl);
               }
@@ -1110,6 +1119,7 @@ BFSIM_UNROLL_W
           if (lane == 0) st_release(&s_ctr[1], hi);
         }
       }
+      if (tie) ntie = true;
     }
     cons += static_cast<unsigned>(D);
     __syncwarp();

@@ -181,6 +181,22 @@ class InputPool:
         self.records = np.ascontiguousarray(self.records, dt)
         self.inputs = np.array(infos, abi.input_dtype) if infos else np.zeros(0, abi.input_dtype)
         self.class_base = np.concatenate(cbs).astype(np.int32) if cbs else np.zeros(1, np.int32)
+        self._arrays = arrays
+
+    def add_prefix(self, i, length):
+        """A further input: the first `length` records of input i, sharing its
+        records (no copy) with its own statistics and class_base. A
+        run_overloaded stream is prefix-stable (the draws of mt19937_64(seed)
+        in order), so a small-G scenario can run on a short prefix of the
+        stream a large-G one needs, and the engine sizes its per-trajectory
+        class deques by the input it runs on. Returns the new input id."""
+        length = int(min(length, self.inputs[i]["length"]))
+        info, cb = prepare(self._arrays[i][:length])
+        info["offset"] = self.inputs[i]["offset"]
+        info["class_base_offset"] = self.class_base.shape[0]
+        self.inputs = np.concatenate([self.inputs, np.array([info], abi.input_dtype)])
+        self.class_base = np.concatenate([self.class_base, cb.astype(np.int32)])
+        return self.inputs.shape[0] - 1
 
 
 class _GenSpec(C.Structure):

@@ -119,3 +119,21 @@ def test_no_gpu_context_fails_loudly():
         pass
     with pytest.raises(host.BfsimError):
         host.Context(0)
+
+
+def test_input_pool_prefix():
+    """InputPool.add_prefix: a stream prefix shares the records and carries the
+    statistics and class_base of the prefix itself (the bench's C4 runs small
+    G on prefixes of the large-G streams)."""
+    s1 = host.sample_stream(3, 5000, s_max=64, p=0.02)
+    s2 = host.sample_stream(4, 3000, s_max=16, p=0.1)
+    pool = host.InputPool([s1, s2])
+    n_rec = pool.records.shape[0]
+    i = pool.add_prefix(1, 700)
+    assert pool.records.shape[0] == n_rec and i == 2
+    info, cb = host.prepare(s2[:700])
+    got = pool.inputs[i]
+    assert int(got["offset"]) == int(pool.inputs[1]["offset"]) and int(got["length"]) == 700
+    assert int(got["s_max"]) == int(info["s_max"]) and int(got["max_decode"]) == int(info["max_decode"])
+    o = int(got["class_base_offset"])
+    assert np.array_equal(pool.class_base[o:o + cb.shape[0]], cb)

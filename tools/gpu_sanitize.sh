@@ -5,10 +5,14 @@
 mkdir -p gpurun_out
 OUT=gpurun_out/sanitizer.txt
 : > $OUT
+CS=/usr/local/cuda/bin/compute-sanitizer
 run() {  # tool, label, command...
   local tool=$1 label=$2; shift 2
+  local log=gpurun_out/san_${tool}_$(echo $label | cut -c1-8 | tr -c 'a-z0-9\n' '_').log
   echo "== $tool: $label" >> $OUT
-  timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 10 "$@" 2>&1 | grep -E "SUMMARY|Error|error|ok|smoke|No such|not found" | tail -4 >> $OUT
+  timeout 900 $CS --tool $tool --print-limit 10 "$@" > $log 2>&1
+  echo "   exit $?" >> $OUT
+  grep -E "SUMMARY|rror|smoke ok|traj" $log | tail -4 >> $OUT
 }
 for tool in memcheck racecheck synccheck; do
   run $tool "smoke (fcfs, jsq, greedy H=0/4, noisy H=8, calendar, overloaded)" python -c "import __graft_entry__ as g; g.smoke()"
