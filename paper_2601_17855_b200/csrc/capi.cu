@@ -325,7 +325,9 @@ void make_plan(Group& g, const bfsim_scenario_t* scen, const bfsim_input_t* inpu
   }
   if (greedy && wpl >= 16) items.push_back({&p.o_key, static_cast<int64_t>(wpl) * 32 * 8, false});
   // M, T, w of the lookahead chain
-  if (greedy && H > 0) items.push_back({&p.o_M, std::max<int64_t>(3 * (H + 1) * 8LL, 128), true});
+  // (the int32 chain keeps only its T row there: H + 1 int32 rounded up to 4)
+  if (greedy && H > 0)
+    items.push_back({&p.o_M, g.hr >= 8 ? ((H + 4) & ~3) * 4LL : std::max<int64_t>(3 * (H + 1) * 8LL, 128), true});
   if (g.noisy) {
     // the draw ring, the draw pass's shared-memory atomics (int32 difference
     // arrays over h) and the int32 chain's [h][g] views

@@ -673,7 +673,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   int2* s_E = NOISY ? gat<int2>(ws, pl.o_lst) : nullptr;
   const uint64_t lkeep = NOISY ? l2_keep_policy() : 0;
   int32_t* s_Eid = NOISY ? gat<int32_t>(ws, pl.o_eid) : nullptr;
-  int32_t* s_pre = NOISY ? at<true, int32_t>(sm, ws, pl.o_pre) : nullptr;
+  int32_t* s_len = NOISY ? at<true, int32_t>(sm, ws, pl.o_pre) : nullptr;  // noisy: per-worker list lengths
   int32_t* n_Wa = NOISY ? reinterpret_cast<int32_t*>(s_Wa) : nullptr;
   int32_t* o_nz = NOISY ? at<SM, int32_t>(sm, ws, pl.o_onz) : nullptr;
   int32_t* nzb = NOISY ? gat<int32_t>(ws, pl.o_nzb) : nullptr;
@@ -690,6 +690,7 @@ __device__ void run_traj(const KParams& P, int si, unsigned char* sm, unsigned c
   for (int i = lane; i < G; i += 32) {
     s_cap[i] = B;
     s_asum[i] = 0;
+    if constexpr (NOISY) s_len[i] = 0;
   }
   if (lane == 0) s_misc[0] = 0;
   constexpr bool kClasses = GREEDY || OVL;
@@ -1036,31 +1037,22 @@ BFSIM_UNROLL_W
   // worker_views -- g ascending, insertion order, engine.hpp:204-220 -- then
   // waiting_views in waiting order, :222-231), taken from the producer
   // warp's ring (draws cons .. cons + D - 1 of the trajectory's stream).
-  // With `values`, active draw r (< act) goes straight into the lookahead
-  // views: it belongs to entry r - pre[g] of worker g's insertion-ordered
-  // list (s_pre: exclusive prefix of the active counts), whose
-  // {finish step, a} the lanes read coalesced (consecutive draws, consecutive
-  // entries), and the request's preview (make_preview, policies.hpp:67-90) is
-  // added to the worker's difference arrays over h with shared-memory
-  // atomics: w_i + d*h while h < min(c_i, rem_i), its last workload a + d*f
-  // while rem_i <= h < c_i, with c_i = min(max(1, rem_i + lround(n_i)), H + 1)
-  // and rem_i = f - k + 1. A waiting draw's value is kept (nzb[r]) only when
-  // its request is admitted this step.
+  // With `values`, the active draws go straight into the lookahead views:
+  // the warp walks each worker's insertion-ordered list {finish step, a}
+  // (32 entries per chunk, coalesced, the next chunk in flight). Retirement
+  // leaves finished entries in place (finish < k); the walk skips them,
+  // numbers the live ones by ballot (draw = running count + rank), and
+  // compacts the list as it goes -- one pass over the lists per step instead
+  // of a compaction pass at retirement and a draw pass here. s_len[g] is the
+  // list length (live entries + not yet dropped finished ones). Each live
+  // request's preview (make_preview, policies.hpp:67-90) is added to the
+  // worker's difference arrays over h with shared-memory atomics:
+  // w_i + d*h while h < min(c_i, rem_i), its last workload a + d*f while
+  // rem_i <= h < c_i, with c_i = min(max(1, rem_i + lround(n_i)), H + 1) and
+  // rem_i = f - k + 1. A waiting draw's value is kept (nzb[r]) only when its
+  // request is admitted this step.
   auto gen_normals = [&](long long D, bool values) {
     if (values) {
-      // the list entry of this lane's next active draw is fetched one chunk
-      // ahead (worker search from the lane's last worker: draws only move
-      // forward)
-      int gq = 0, gn = 0;
-      int2 en = make_int2(0, 0);
-      auto fetch = [&](long long r) {
-        int g = gq, nx = s_pre[g + 1];
-        while (nx <= r) nx = s_pre[++g + 1];
-        gq = g;
-        gn = g;
-        en = ld_keep(s_E + g * B + static_cast<int>(r - s_pre[g]), lkeep);
-      };
-      if (lane < act) fetch(lane);
       // loop-local copies (the kernel-wide ones live in spilled registers) and
       // 32-bit arithmetic: every quantity below is a step count, a clamped
       // draw or a per-request workload, all < 2^31 (capi.cu bounds)
@@ -1068,52 +1060,92 @@ BFSIM_UNROLL_W
       const int32_t kk32 = static_cast<int32_t>(k), d32 = static_cast<int32_t>(d), H1 = H + 1;
       const int32_t dk32 = static_cast<int32_t>(d * k);
       unsigned tie = 0;
-      for (long long r0 = 0; r0 < D; r0 += 32) {
-        const long long r = r0 + lane;
-        const int gc = gn;
-        const int2 ec = en;
-        if (r + 32 < act) fetch(r + 32);
-        bool need = r < D;
-        if (need && r >= act) {
-          const long long p = r - act;
-          need = (__ldcg(selb + (p >> 5)) >> (p & 31)) & 1u;
+      // wait until the producer has published draws [.., cn + hi)
+      auto wait_draws = [&](unsigned hi) {
+        for (int spin = 0; static_cast<int>(ld_acquire(&s_ctr[0]) - hi) < 0; ++spin) {
+          if (spin > (1 << 26)) __trap();  // the producer never stalls this long: fail, do not hang
+          __nanosleep(32);
         }
-        if (__any_sync(FULLMASK, need)) {
-          // everything before r0 is consumed: release it first (the producer
-          // may be waiting for room), then wait for this chunk's draws
-          if (lane == 0) st_release(&s_ctr[1], cn + static_cast<unsigned>(r0));
-          const unsigned hi = cn + static_cast<unsigned>(r0 + 32 < D ? r0 + 32 : D);
-          for (int spin = 0; static_cast<int>(ld_acquire(&s_ctr[0]) - hi) < 0; ++spin) {
-            if (spin > (1 << 26)) __trap();  // the producer never stalls this long: fail, do not hang
-            __nanosleep(32);
-          }
-          if (need) {
-            const int code = s_ring[(cn + static_cast<unsigned>(r)) & (kRing - 1)];
+      };
+      // ---- active draws: worker lists in g order
+      int g = 0, len = G > 0 ? s_len[0] : 0;
+      while (len == 0 && ++g < G) len = s_len[g];
+      int2 ecur = g < G && lane < len ? ld_keep(s_E + g * B + lane, lkeep) : make_int2(0, 0);
+      int p0 = 0, wpos = 0;
+      unsigned rb = 0;  // active draws taken so far
+      while (g < G) {
+        // the next chunk (this worker's next 32 entries, else the next
+        // non-empty worker's first), loaded before this chunk's stores
+        int g2 = g, p2 = p0 + 32, len2 = len;
+        if (p2 >= len) {
+          p2 = 0;
+          len2 = 0;
+          while (len2 == 0 && ++g2 < G) len2 = s_len[g2];
+        }
+        const int2 enx = g2 < G && p2 + lane < len2 ? ld_keep(s_E + g2 * B + p2 + lane, lkeep) : make_int2(0, 0);
+        const int p = p0 + lane;
+        const bool live = p < len && ecur.x >= kk32;
+        const unsigned lm = __ballot_sync(FULLMASK, live);
+        const int nl = __popc(lm);
+        if (nl) {
+          const int rk = __popc(lm & lanemask_lt());
+          if (lane == 0) st_release(&s_ctr[1], cn + rb);  // the producer may be waiting for room
+          wait_draws(cn + rb + static_cast<unsigned>(nl));
+          if (live) {
+            const int code = s_ring[(cn + rb + static_cast<unsigned>(rk)) & (kRing - 1)];
             const int32_t lr = code >> 1;
             tie |= static_cast<unsigned>(code) & 1u;
-            if (r >= act) {
-              nzb[r] = lr;
-            } else {
-              const int g = gc;
-              const int32_t f = ec.x;
-              const int32_t a = ec.y;
-              const int32_t rem = f - kk32 + 1;
-              int32_t pred = rem + lr;
-              pred = pred > 1 ? pred : 1;
-              const int32_t c = pred < H1 ? pred : H1;
-              const int32_t m = c < rem ? c : rem;
-              if (m <= H) {
-                atomicAdd(&n_Wa[(m - 1) * G + g], -(a + dk32));
-                atomicAdd(&s_Wc[(m - 1) * G + g], -1);
-              }
-              if (c > rem) {
-                // the last workload a + d*f < 2^31; the product alone may not be
-                const int32_t wl = static_cast<int32_t>(static_cast<uint32_t>(a) +
-                                                        static_cast<uint32_t>(d32) * static_cast<uint32_t>(f));
-                atomicAdd(&n_Wa[(rem - 1) * G + g], wl);
-                if (c <= H) atomicAdd(&n_Wa[(c - 1) * G + g], -wl);
-              }
+            const int32_t f = ecur.x;
+            const int32_t a = ecur.y;
+            const int32_t rem = f - kk32 + 1;
+            int32_t pred = rem + lr;
+            pred = pred > 1 ? pred : 1;
+            const int32_t c = pred < H1 ? pred : H1;
+            const int32_t m = c < rem ? c : rem;
+            if (m <= H) {
+              atomicAdd(&n_Wa[(m - 1) * G + g], -(a + dk32));
+              atomicAdd(&s_Wc[(m - 1) * G + g], -1);
             }
+            if (c > rem) {
+              // the last workload a + d*f < 2^31; the product alone may not be
+              const int32_t wl = static_cast<int32_t>(static_cast<uint32_t>(a) +
+                                                      static_cast<uint32_t>(d32) * static_cast<uint32_t>(f));
+              atomicAdd(&n_Wa[(rem - 1) * G + g], wl);
+              if (c <= H) atomicAdd(&n_Wa[(c - 1) * G + g], -wl);
+            }
+            // compaction in place (an entry only moves down; the next chunk
+            // is already loaded)
+            if (wpos + rk != p) st_keep(s_E + g * B + wpos + rk, ecur, lkeep);
+          }
+          rb += static_cast<unsigned>(nl);
+          wpos += nl;
+        }
+        if (g2 != g) {
+          if (lane == 0) s_len[g] = wpos;
+          wpos = 0;
+        }
+        g = g2;
+        p0 = p2;
+        len = len2;
+        ecur = enx;
+      }
+      __syncwarp();
+      // ---- waiting draws (r >= act): only the admitted ranks' values matter
+      for (long long r0 = act; r0 < D; r0 += 32) {
+        const long long r = r0 + lane;
+        bool need = r < D;
+        if (need) {
+          const long long q = r - act;
+          need = (__ldcg(selb + (q >> 5)) >> (q & 31)) & 1u;
+        }
+        if (__any_sync(FULLMASK, need)) {
+          if (lane == 0) st_release(&s_ctr[1], cn + static_cast<unsigned>(r0));
+          const unsigned hi = cn + static_cast<unsigned>(r0 + 32 < D ? r0 + 32 : D);
+          wait_draws(hi);
+          if (need) {
+            const int code = s_ring[(cn + static_cast<unsigned>(r)) & (kRing - 1)];
+            tie |= static_cast<unsigned>(code) & 1u;
+            nzb[r] = code >> 1;
           }
           __syncwarp();
           if (lane == 0) st_release(&s_ctr[1], hi);
@@ -1151,27 +1183,6 @@ BFSIM_UNROLL_W
       out[q] = rank;
       atomicOr(selb + (rank >> 5), 1u << (rank & 31));
     }
-    __syncwarp();
-  };
-
-  // Draw r -> worker: s_pre[g] = active requests of workers < g (their
-  // draws come first, worker_views g ascending, engine.hpp:204-220).
-  auto noisy_pre = [&]() {
-    long long base = 0;
-BFSIM_UNROLL_W
-    for (int j = 0; j < WPL; ++j) {
-      const int g = lane + 32 * j;
-      const int v = g < G ? n[j] : 0;
-      int incl = v;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int t = __shfl_up_sync(FULLMASK, incl, off);
-        if (lane >= off) incl += t;
-      }
-      if (g < G) s_pre[g] = static_cast<int>(base) + incl - v;
-      base += __shfl_sync(FULLMASK, incl, 31);
-    }
-    if (lane == 0) s_pre[G] = static_cast<int>(base);
     __syncwarp();
   };
 
@@ -1680,7 +1691,6 @@ BFSIM_UNROLL_W
         // active draws build the views' difference arrays, each admitted
         // request keeps its own waiting draw
         waiting_ranks(U, o_id, o_nz);
-        noisy_pre();
         gen_normals(act + n_wait, true);
         if constexpr (HR == 0) noisy_views();
         for (int q = lane; q < U; q += 32) {
@@ -1801,11 +1811,9 @@ BFSIM_UNROLL_W
           int gs = static_cast<int>(wmin(fk) & static_cast<key_t>(gmask));
           int32_t Fg = hl ? s_F32[gs * HP + lane] : 0;
           if (__any_sync(FULLMASK, hl && Fg + wl > Ml)) {
-            // T_h = M_h - w_h (zero past H, like the rows) to the T row,
-            // then every lane scans its workers' rows 4 horizons per load
-            int32_t* s_T = reinterpret_cast<int32_t*>(s_M);  // the shared chain's M/T/w rows are unused here
-            if (lane < HP) s_T[lane] = hl ? Ml - wl : 0;
-            __syncwarp();
+            // T_h = M_h - w_h from lane h (zero past H, like the rows); every
+            // lane scans its workers' rows 4 horizons per 128-bit load
+            const int32_t Tl = Ml - wl;
             uint32_t cost[WPL];
 BFSIM_UNROLL_W
             for (int j = 0; j < WPL; ++j) cost[j] = 0;
@@ -1813,7 +1821,11 @@ BFSIM_UNROLL_W
 #pragma unroll
             for (int h4 = 0; h4 < HP4MAX; ++h4) {
               if (h4 < nh4) {
-                const int4 T = reinterpret_cast<const int4*>(s_T)[h4];
+                int4 T;
+                T.x = __shfl_sync(FULLMASK, Tl, 4 * h4);
+                T.y = __shfl_sync(FULLMASK, Tl, 4 * h4 + 1);
+                T.z = __shfl_sync(FULLMASK, Tl, 4 * h4 + 2);
+                T.w = __shfl_sync(FULLMASK, Tl, 4 * h4 + 3);
 BFSIM_UNROLL_W
                 for (int j = 0; j < WPL; ++j) {
                   const int g = lane + 32 * j;
@@ -2036,6 +2048,7 @@ BFSIM_UNROLL_W
           const int g = lane + 32 * j;
           if (g >= G) continue;
           const int base = g * B + n[j];
+          s_len[g] = n[j] + adm[j];  // the draw pass compacted the list to n[j] live entries
           for (int t = 1; t < adm[j]; ++t) {
             const int key = s_Eid[base + t];
             const int2 ev = s_E[base + t];
@@ -2173,39 +2186,9 @@ BFSIM_UNROLL_W
         }
       }
       __syncwarp();
-      if constexpr (NOISY) {
-        // erase_if keeps insertion order (engine.hpp:118-120): each worker
-        // with completions compacts its list, the whole warp over its
-        // entries (coalesced), dropping the ones that finish at step k
-BFSIM_UNROLL_W
-        for (int j = 0; j < WPL; ++j) {
-          unsigned dm = __ballot_sync(FULLMASK, lane + 32 * j < G && rc[j] > 0);
-          while (dm) {
-            const int src = __ffs(dm) - 1;
-            dm &= dm - 1;
-            const int g = src + 32 * j;
-            const int nold = __shfl_sync(FULLMASK, n[j], src);
-            int2* Eg = s_E + g * B;
-            int w = 0;
-            for (int p0 = 0; p0 < nold; p0 += 64) {  // two chunks in flight
-              const int p = p0 + lane, p2 = p0 + 32 + lane;
-              const int2 e = p < nold ? ld_keep(Eg + p, lkeep) : make_int2(0, 0);
-              const int2 e2 = p2 < nold ? ld_keep(Eg + p2, lkeep) : make_int2(0, 0);
-              const bool keep = p < nold && static_cast<uint32_t>(e.x) != kf;
-              const bool keep2 = p2 < nold && static_cast<uint32_t>(e2.x) != kf;
-              const unsigned km = __ballot_sync(FULLMASK, keep);
-              const unsigned km2 = __ballot_sync(FULLMASK, keep2);
-              // in place: an entry moves only to a lower position, and the
-              // second chunk's reads are done before any store
-              if (keep) st_keep(Eg + w + __popc(km & lanemask_lt()), e, lkeep);
-              w += __popc(km);
-              if (keep2) st_keep(Eg + w + __popc(km2 & lanemask_lt()), e2, lkeep);
-              w += __popc(km2);
-            }
-          }
-        }
-        __syncwarp();
-      }
+      // noisy: erase_if keeps insertion order (engine.hpp:118-120); the
+      // finished entries stay in the worker lists until the next draw pass
+      // walks and compacts them (gen_normals)
 BFSIM_UNROLL_W
       for (int j = 0; j < WPL; ++j) {
         const int g = lane + 32 * j;

@@ -201,7 +201,7 @@ def test_overloaded_random_batch(ctx, orc):
 def test_rejections(ctx):
     tr = host.sample_instance(3, rate=100.0, duration=1.0)
     pool = host.InputPool([tr])
-    for bad in (dict(policy=abi.BFIO_EXACT), dict(drift=0.5), dict(drift=-1.0), dict(workers=0),
+    for bad in (dict(policy=abi.BFIO_EXACT), dict(drift=0.1), dict(drift=-1.0), dict(workers=0),
                 dict(gamma=1.0), dict(per_token=0.0)):
         with pytest.raises(host.InvalidArgument):
             ctx.run_batch(np.array([abi.scenario(**bad)], abi.scenario_dtype), pool)
