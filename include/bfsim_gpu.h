@@ -116,8 +116,9 @@ typedef struct bfsim_scenario_t {
   int32_t batch;     /* B */
   int32_t horizon;   /* H */
   int32_t input_id;  /* index into the bfsim_input_t table */
-  int32_t reserved0;
-  double drift;       /* DriftSpec::constant(value); must be a non-negative integer */
+  int32_t reserved0;  /* ignored on input (the library's dyadic-drift shift) */
+  double drift;       /* DriftSpec::constant(value): a non-negative integer, or dyadic m / 2^e
+                         (e <= 16, s_max * 2^e <= 262143), exact like the reference's fp64 profile */
   double overhead;    /* C     */
   double per_token;   /* t_ell */
   double noise_sigma; /* Noisy lookahead sigma */
@@ -144,8 +145,9 @@ typedef struct bfsim_result_t {
   int64_t completed;  /* completed requests (overloaded: includes warm-up) */
   int64_t admitted;   /* admitted requests */
   int64_t consumed;   /* overloaded: samples drawn from the stream */
-  int64_t imb_total_i;      /* exact integer sum of G*max - sum over records */
-  int64_t total_workload_i; /* exact integer sum of loads over records */
+  int64_t imb_total_i;      /* exact integer sum of G*max - sum over records (dyadic drift m / 2^e:
+                               in units of 2^-e) */
+  int64_t total_workload_i; /* exact integer sum of loads over records (same units) */
   int64_t tokens_i;         /* exact sum of active_count over records */
   double avg_imbalance, throughput, tpot, energy, imb_total, total_workload, eta_sum;
   double clock;   /* simulated clock after the last step */
