@@ -1067,22 +1067,36 @@ BFSIM_UNROLL_W
           __nanosleep(32);
         }
       };
-      // ---- active draws: worker lists in g order
-      int g = 0, len = G > 0 ? s_len[0] : 0;
-      while (len == 0 && ++g < G) len = s_len[g];
-      int2 ecur = g < G && lane < len ? ld_keep(s_E + g * B + lane, lkeep) : make_int2(0, 0);
-      int p0 = 0, wpos = 0;
-      unsigned rb = 0;  // active draws taken so far
-      while (g < G) {
-        // the next chunk (this worker's next 32 entries, else the next
-        // non-empty worker's first), loaded before this chunk's stores
-        int g2 = g, p2 = p0 + 32, len2 = len;
+      // ---- active draws: worker lists in g order, 32 entries per chunk,
+      // the next two chunks' loads in flight (the lists live in L2 / HBM)
+      auto next_chunk = [&](int g, int p0, int len, int& g2, int& p2, int& len2) {
+        g2 = g;
+        p2 = p0 + 32;
+        len2 = len;
         if (p2 >= len) {
           p2 = 0;
           len2 = 0;
           while (len2 == 0 && ++g2 < G) len2 = s_len[g2];
         }
-        const int2 enx = g2 < G && p2 + lane < len2 ? ld_keep(s_E + g2 * B + p2 + lane, lkeep) : make_int2(0, 0);
+      };
+      auto load_chunk = [&](int g, int p0, int len) {
+        return g < G && p0 + lane < len ? ld_keep(s_E + g * B + p0 + lane, lkeep) : make_int2(0, 0);
+      };
+      int g = -1, len = 0;
+      while (len == 0 && ++g < G) len = s_len[g];
+      int p0 = 0;
+      int g2, p2, len2;
+      next_chunk(g, p0, len, g2, p2, len2);
+      int2 ecur = load_chunk(g, p0, len);
+      int2 enx = load_chunk(g2, p2, len2);
+      int wpos = 0;
+      unsigned rb = 0;  // active draws taken so far
+      while (g < G) {
+        // the chunk after next, loaded before this chunk's stores (an entry
+        // only moves down within its worker's row)
+        int g3, p3, len3;
+        next_chunk(g2, p2, len2, g3, p3, len3);
+        const int2 enn = load_chunk(g3, p3, len3);
         const int p = p0 + lane;
         const bool live = p < len && ecur.x >= kk32;
         const unsigned lm = __ballot_sync(FULLMASK, live);
@@ -1128,6 +1142,10 @@ BFSIM_UNROLL_W
         p0 = p2;
         len = len2;
         ecur = enx;
+        g2 = g3;
+        p2 = p3;
+        len2 = len3;
+        enx = enn;
       }
       __syncwarp();
       // ---- waiting draws (r >= act): only the admitted ranks' values matter
@@ -1785,6 +1803,16 @@ BFSIM_UNROLL_W
         __syncwarp();
         const int32_t d32 = static_cast<int32_t>(d);
         const int32_t dl = d32 * lane;
+        // F_0 and the free slots of the lane's workers stay in registers
+        // across the items (only the chosen worker's change: F_0 += w_0 = c,
+        // one slot less), so the per-item fast-path key needs no shared loads
+        int32_t F0r[WPL], capr[WPL];
+BFSIM_UNROLL_W
+        for (int j = 0; j < WPL; ++j) {
+          const int g = lane + 32 * j;
+          F0r[j] = g < G ? s_F32[g * HP] : 0;
+          capr[j] = g < G ? s_cap[g] : 0;
+        }
         for (int q = 0; q < U; ++q) {
           int c, o;
           long long lim;
@@ -1803,8 +1831,8 @@ BFSIM_UNROLL_W
 BFSIM_UNROLL_W
           for (int j = 0; j < WPL; ++j) {
             const int g = lane + 32 * j;
-            F0v[j] = g < G ? s_F32[g * HP] : 0;
-            fre[j] = g < G && s_cap[g] > 0;
+            F0v[j] = F0r[j];
+            fre[j] = capr[j] > 0;
             const key_t kk = (static_cast<key_t>(static_cast<uint32_t>(F0v[j])) << gbits) | static_cast<key_t>(g);
             if (fre[j] && kk < fk) fk = kk;
           }
@@ -1854,6 +1882,12 @@ BFSIM_UNROLL_W
             s_F32[gs * HP + lane] = v;
             Ml = v > Ml ? v : Ml;
           }
+BFSIM_UNROLL_W
+          for (int j = 0; j < WPL; ++j)
+            if (lane + 32 * j == gs) {
+              F0r[j] += c;
+              capr[j] -= 1;
+            }
           if (lane == (gs & 31)) {
             const int rank = s_admc[gs];
             s_admc[gs] = rank + 1;
