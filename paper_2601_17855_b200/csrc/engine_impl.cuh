@@ -1082,21 +1082,27 @@ BFSIM_UNROLL_W
       auto load_chunk = [&](int g, int p0, int len) {
         return g < G && p0 + lane < len ? ld_keep(s_E + g * B + p0 + lane, lkeep) : make_int2(0, 0);
       };
-      int g = -1, len = 0;
-      while (len == 0 && ++g < G) len = s_len[g];
-      int p0 = 0;
-      int g2, p2, len2;
-      next_chunk(g, p0, len, g2, p2, len2);
-      int2 ecur = load_chunk(g, p0, len);
-      int2 enx = load_chunk(g2, p2, len2);
+      constexpr int PF = 3;  // chunks in flight (the one being processed + PF - 1 ahead)
+      int cg[PF], cp[PF], cl[PF];
+      int2 ce[PF];
+      cg[0] = -1;
+      cl[0] = 0;
+      cp[0] = 0;
+      while (cl[0] == 0 && ++cg[0] < G) cl[0] = s_len[cg[0]];
+#pragma unroll
+      for (int i = 1; i < PF; ++i) next_chunk(cg[i - 1], cp[i - 1], cl[i - 1], cg[i], cp[i], cl[i]);
+#pragma unroll
+      for (int i = 0; i < PF; ++i) ce[i] = load_chunk(cg[i], cp[i], cl[i]);
       int wpos = 0;
       unsigned rb = 0;  // active draws taken so far
-      while (g < G) {
-        // the chunk after next, loaded before this chunk's stores (an entry
+      while (cg[0] < G) {
+        // the next chunk in line, loaded before this chunk's stores (an entry
         // only moves down within its worker's row)
-        int g3, p3, len3;
-        next_chunk(g2, p2, len2, g3, p3, len3);
-        const int2 enn = load_chunk(g3, p3, len3);
+        int gN, pN, lN;
+        next_chunk(cg[PF - 1], cp[PF - 1], cl[PF - 1], gN, pN, lN);
+        const int2 eN = load_chunk(gN, pN, lN);
+        const int g = cg[0], p0 = cp[0], len = cl[0];
+        const int2 ecur = ce[0];
         const int p = p0 + lane;
         const bool live = p < len && ecur.x >= kk32;
         const unsigned lm = __ballot_sync(FULLMASK, live);
@@ -1134,18 +1140,21 @@ BFSIM_UNROLL_W
           rb += static_cast<unsigned>(nl);
           wpos += nl;
         }
-        if (g2 != g) {
+        if (cg[1] != g) {
           if (lane == 0) s_len[g] = wpos;
           wpos = 0;
         }
-        g = g2;
-        p0 = p2;
-        len = len2;
-        ecur = enx;
-        g2 = g3;
-        p2 = p3;
-        len2 = len3;
-        enx = enn;
+#pragma unroll
+        for (int i = 0; i + 1 < PF; ++i) {
+          cg[i] = cg[i + 1];
+          cp[i] = cp[i + 1];
+          cl[i] = cl[i + 1];
+          ce[i] = ce[i + 1];
+        }
+        cg[PF - 1] = gN;
+        cp[PF - 1] = pN;
+        cl[PF - 1] = lN;
+        ce[PF - 1] = eN;
       }
       __syncwarp();
       // ---- waiting draws (r >= act): only the admitted ranks' values matter
