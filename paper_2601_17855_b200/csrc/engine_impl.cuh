@@ -1061,12 +1061,19 @@ BFSIM_UNROLL_W
       const int32_t dk32 = static_cast<int32_t>(d * k);
       unsigned tie = 0;
       // wait until the producer has published draws [.., cn + hi)
+      // (returns the producer count it saw, warp-uniform)
       auto wait_draws = [&](unsigned hi) {
-        for (int spin = 0; static_cast<int>(ld_acquire(&s_ctr[0]) - hi) < 0; ++spin) {
+        unsigned seen;
+        for (int spin = 0; static_cast<int>((seen = ld_acquire(&s_ctr[0])) - hi) < 0; ++spin) {
           if (spin > (1 << 26)) __trap();  // the producer never stalls this long: fail, do not hang
           __nanosleep(32);
         }
+        return __shfl_sync(FULLMASK, seen, 0);
       };
+      // the active walk re-reads the producer count only when the draws it
+      // saw run out, and releases consumed draws every 256 (a release store
+      // orders all of lane 0's earlier memory operations: not per chunk)
+      unsigned avail = cn, relp = 0;
       // ---- active draws: worker lists in g order, 32 entries per chunk,
       // the next two chunks' loads in flight (the lists live in L2 / HBM)
       auto next_chunk = [&](int g, int p0, int len, int& g2, int& p2, int& len2) {
@@ -1109,8 +1116,15 @@ BFSIM_UNROLL_W
         const int nl = __popc(lm);
         if (nl) {
           const int rk = __popc(lm & lanemask_lt());
-          if (lane == 0) st_release(&s_ctr[1], cn + rb);  // the producer may be waiting for room
-          wait_draws(cn + rb + static_cast<unsigned>(nl));
+          const unsigned need = cn + rb + static_cast<unsigned>(nl);
+          if (static_cast<int>(avail - need) < 0) {
+            if (lane == 0) st_release(&s_ctr[1], cn + rb);  // the producer may be waiting for room
+            relp = rb;
+            avail = wait_draws(need);
+          } else if (rb - relp >= 256u) {
+            if (lane == 0) st_release(&s_ctr[1], cn + rb);
+            relp = rb;
+          }
           if (live) {
             const int code = s_ring[(cn + rb + static_cast<unsigned>(rk)) & (kRing - 1)];
             const int32_t lr = code >> 1;
